@@ -1,0 +1,359 @@
+"""Pins for the float64 CPU oracle (-m "not gpu").
+
+Each test checks oracle/flr_ref.c against something OTHER than itself: raw-pixel
+brute-force least squares (tests/brute.py), closed forms derived by hand, the
+paper's stated limits, exact invariances, and the cited golden fixture.  The
+pin ids P1..P12 follow SURVEY.md section 8(c).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from tests import brute
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rand_planes(rng, Q, H, W, lo=0.0, hi=1.0):
+    return rng.uniform(lo, hi, size=(Q, H, W)).astype(np.float32)
+
+
+# ---------------------------------------------------------------- P1: K1 closed form
+def test_p1_constant_block_moments(oracle_mod):
+    """A constant D x D block (g, y) has n = D^2, u = D^2 g, S = D^2 g g^T, N_0 = D^2 y
+    (SPEC S:312)."""
+    D, Q = 8, 3
+    g = np.array([0.25, -0.5, 0.75], dtype=np.float32)
+    y = np.array([0.1, 0.2, 0.3], dtype=np.float32)
+    G = np.broadcast_to(g[:, None, None], (Q, D, D)).copy()
+    Y = np.broadcast_to(y[:, None, None], (3, D, D)).copy()
+    M, N = oracle_mod.moments(G, Y, D)
+    xt = np.concatenate([[1.0], g.astype(np.float64)])
+    assert M.shape == (1, 1, 1, Q + 1, Q + 1)
+    np.testing.assert_allclose(M[0, 0, 0], D * D * np.outer(xt, xt), rtol=1e-15)
+    np.testing.assert_allclose(N[0, 0, 0], D * D * np.outer(xt, y.astype(np.float64)), rtol=1e-15)
+
+
+def test_p1_truncated_edge_blocks(oracle_mod):
+    """Edge blocks are truncated (R5): n counts only in-image pixels."""
+    rng = np.random.default_rng(1)
+    G = rand_planes(rng, 2, 11, 13)
+    Y = rand_planes(rng, 3, 11, 13)
+    M, N = oracle_mod.moments(G, Y, 4)
+    assert M.shape[1:3] == (3, 4)
+    counts = M[0, :, :, 0, 0]
+    np.testing.assert_array_equal(counts, [[16, 16, 16, 4], [16, 16, 16, 4], [12, 12, 12, 3]])
+    # a plain numpy sum over the same pixels
+    np.testing.assert_allclose(N[0, 2, 3, 0], Y[:, 8:11, 12:13].astype(np.float64).sum((1, 2)), rtol=1e-14)
+    np.testing.assert_allclose(M[0, 1, 2, 1, 2],
+                               (G[0, 4:8, 8:12].astype(np.float64) * G[1, 4:8, 8:12]).sum(), rtol=1e-14)
+
+
+# ---------------------------------------------------------------- P2: K2 blur
+def test_p2_blur_impulse_response(oracle_mod):
+    """An impulse in the moment field spreads as g_dy g_dx with g_i = exp(-i^2/2s^2)
+    (P:299-300), zero outside |d| <= R, truncated at the grid edge (R3)."""
+    P, By, Bx, s, R = 2, 9, 11, 1.25, 3
+    M = np.zeros((1, By, Bx, P, P))
+    N = np.zeros((1, By, Bx, P, 3))
+    M[0, 4, 2, 0, 0] = 1.0
+    N[0, 4, 2, 1, 2] = 2.0
+    Mb, Nb = oracle_mod.blur(M, N, s, R)
+    for by in range(By):
+        for bx in range(Bx):
+            dy, dx = by - 4, bx - 2
+            w = math.exp(-dy * dy / (2 * s * s)) * math.exp(-dx * dx / (2 * s * s)) \
+                if abs(dy) <= R and abs(dx) <= R else 0.0
+            assert Mb[0, by, bx, 0, 0] == pytest.approx(w, rel=1e-14, abs=1e-300)
+            assert Nb[0, by, bx, 1, 2] == pytest.approx(2 * w, rel=1e-14, abs=1e-300)
+    assert np.count_nonzero(Mb) == 6 * 7  # columns -1..5 clipped to 0..5, rows 1..7
+
+
+def test_p2_taps(oracle_mod):
+    g = oracle_mod.gauss_taps(1.25, 3)
+    np.testing.assert_allclose(g, [math.exp(-i * i / (2 * 1.25 ** 2)) for i in range(-3, 4)], rtol=1e-15)
+
+
+# ---------------------------------------------------------------- P3: whole fit = brute-force WLS
+@pytest.mark.parametrize("D,Q,W,H,sigma,R", [(8, 3, 29, 21, 10.0, 2), (4, 2, 19, 14, 5.0, 3),
+                                             (2, 4, 9, 7, 3.0, 2)])
+def test_p3_fit_equals_bruteforce_wls_unregularised(oracle_mod, D, Q, W, H, sigma, R):
+    """At eps = eps_mul = 0 each block model is the plain weighted LS fit (P:258-270,
+    P:303-307) with pixel weights g(block dy) g(block dx) -- checked by lstsq on pixels."""
+    rng = np.random.default_rng(D * 100 + Q)
+    G = rand_planes(rng, Q, H, W, -1, 1)
+    Y = rand_planes(rng, 3, H, W, 0, 2)
+    A = oracle_mod.fit(G, Y, D=D, sigma=sigma, R=R, eps_add=0.0, eps_mul=0.0)[0]
+    Ab = brute.fit_blocks(G, Y, D, sigma, R, 0.0, 0.0)
+    np.testing.assert_allclose(A, Ab, rtol=1e-9, atol=1e-10)
+
+
+@pytest.mark.parametrize("eps_add,eps_mul", [(1e-5, 1e-4), (1e-2, 0.0), (0.0, 0.3), (0.05, 0.2)])
+def test_p3_fit_equals_bruteforce_ridge(oracle_mod, eps_add, eps_mul):
+    """With regularisation, the appendix model equals the ridge LS minimiser with the
+    penalty derived in tests/brute.py (independent route through P:683-709)."""
+    rng = np.random.default_rng(7)
+    Q, H, W, D = 3, 17, 23, 4
+    G = rand_planes(rng, Q, H, W, 0.2, 0.9)  # non-zero means exercise eps_mul terms
+    Y = rand_planes(rng, 3, H, W, 0, 1)
+    A = oracle_mod.fit(G, Y, D=D, sigma=6.0, R=2, eps_add=eps_add, eps_mul=eps_mul)[0]
+    Ab = brute.fit_blocks(G, Y, D, 6.0, 2, eps_add, eps_mul)
+    np.testing.assert_allclose(A, Ab, rtol=1e-8, atol=1e-9)
+
+
+# ---------------------------------------------------------------- P4: D = 1 = dense windowed regression
+def test_p4_block1_equals_dense_windowed(oracle_mod):
+    """With 1x1 blocks the blocked method IS the per-pixel windowed regression of
+    Fig. 3: per-pixel Gaussian-window moments + the appendix solver."""
+    rng = np.random.default_rng(3)
+    Q, H, W = 2, 9, 11
+    G = rand_planes(rng, Q, H, W)
+    Y = rand_planes(rng, 3, H, W)
+    out = oracle_mod.denoise(G, Y, D=1, sigma=1.5, R=3, eps_add=1e-3, eps_mul=1e-2)[0]
+    ref = brute.dense_windowed(G, Y, 1.5, 3, 1e-3, 1e-2)
+    np.testing.assert_allclose(out, ref, rtol=1e-9, atol=1e-11)
+
+
+# ---------------------------------------------------------------- P5: Q = 1 closed form
+@pytest.mark.parametrize("eps_add,eps_mul", [(1e-5, 1e-4), (0.01, 0.1), (0.0, 0.0)])
+def test_p5_q1_closed_form(oracle_mod, eps_add, eps_mul):
+    """Q = 1 by hand from P:683-716: W^ = var + 2 eps_mul mu^2 + eps_add, C^ = 1,
+    B^ = cov / sigma^, A^ = B^/(1 + eps_add) => slope = cov / ((var + 2 eps_mul mu^2 +
+    eps_add)(1 + eps_add)), bias = mu_Y - slope mu_X.  (He et al.'s guided filter
+    a = cov/(var + eps) when eps_mul = 0, up to the (1 + eps) factor.)"""
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0.3, 0.8, 40)
+    y = rng.uniform(0, 1, (40, 3))
+    w = rng.uniform(0.1, 1.0, 40)
+    M = np.array([[w.sum(), (w * x).sum()], [(w * x).sum(), (w * x * x).sum()]])
+    N = np.stack([(w[:, None] * y).sum(0), (w[:, None] * x[:, None] * y).sum(0)])
+    A = oracle_mod.solve_block(M, N, eps_add, eps_mul)
+    n = w.sum()
+    mu = (w * x).sum() / n
+    muy = (w[:, None] * y).sum(0) / n
+    var = (w * (x - mu) ** 2).sum() / n
+    cov = (w[:, None] * (x - mu)[:, None] * (y - muy)).sum(0) / n
+    slope = cov / ((var + 2 * eps_mul * mu * mu + eps_add) * (1 + eps_add))
+    np.testing.assert_allclose(A[1], slope, rtol=1e-12)
+    np.testing.assert_allclose(A[0], muy - slope * mu, rtol=1e-12, atol=1e-15)
+
+
+# ---------------------------------------------------------------- P6-P8: end-to-end exact cases
+def test_p6_affine_radiance_is_reproduced(oracle_mod):
+    """If Y = X~ A globally and the guides are non-degenerate, the unregularised
+    regression reproduces Y exactly."""
+    rng = np.random.default_rng(11)
+    Q, H, W = 4, 24, 32
+    G = rand_planes(rng, Q, H, W, -1, 1)
+    A_true = rng.normal(size=(Q + 1, 3))
+    Xt = np.concatenate([np.ones((1, H, W)), G.astype(np.float64)])
+    Y = np.einsum("qhw,qc->chw", Xt, A_true)
+    out = oracle_mod.denoise(G, Y.astype(np.float32), D=8, sigma=10.0, R=3, eps_add=0.0, eps_mul=0.0)[0]
+    np.testing.assert_allclose(out, Y.astype(np.float32).astype(np.float64), atol=2e-6)
+    Y64 = np.einsum("qhw,qc->chw", Xt, A_true).astype(np.float32)
+    np.testing.assert_allclose(out, Y64, atol=2e-6)
+
+
+def test_p7_constant_image_maps_to_itself(oracle_mod):
+    """Constant Y = c: B^ = 0, so every model is the bias c, for any eps."""
+    rng = np.random.default_rng(12)
+    G = rand_planes(rng, 5, 20, 27)
+    c = np.array([0.3, 1.7, 0.02], dtype=np.float32)
+    Y = np.broadcast_to(c[:, None, None], (3, 20, 27)).copy()
+    for ea, em in [(1e-5, 1e-4), (0.1, 0.5), (0.0, 0.0)]:
+        out = oracle_mod.denoise(G, Y, D=4, sigma=6.0, R=2, eps_add=ea, eps_mul=em)[0]
+        np.testing.assert_allclose(out, np.broadcast_to(c.astype(np.float64)[:, None, None], out.shape),
+                                   rtol=1e-12)
+
+
+def test_p8_huge_eps_is_a_gaussian_blur(oracle_mod):
+    """eps -> inf interpolates to a Gaussian blur: the output tends to the
+    bilinear blend of Gaussian-weighted block means of Y."""
+    rng = np.random.default_rng(13)
+    Q, H, W, D, s, R = 3, 16, 24, 4, 1.5, 2
+    G = rand_planes(rng, Q, H, W)
+    Y = rand_planes(rng, 3, H, W)
+    out = oracle_mod.denoise(G, Y, D=D, sigma=s * D, R=R, eps_add=1e7, eps_mul=0.0)[0]
+    By, Bx = H // D, W // D
+    means = np.zeros((By, Bx, Q + 1, 3))
+    for by in range(By):
+        for bx in range(Bx):
+            w = brute.block_pixel_weights(W, H, D, bx, by, s, R)
+            means[by, bx, 0] = (w[None] * Y).sum((1, 2)) / w.sum()
+    ref = brute.apply_blend(means, G, D)
+    np.testing.assert_allclose(out, ref, atol=1e-6)
+
+
+# ---------------------------------------------------------------- P9: invariances
+def _scene(rng, Q=4, H=24, W=32):
+    G = rand_planes(rng, Q, H, W, 0.1, 0.9)
+    Y = rand_planes(rng, 3, H, W, 0.0, 1.0)
+    return G, Y
+
+
+def test_p9_guide_permutation_invariance(oracle_mod):
+    rng = np.random.default_rng(21)
+    G, Y = _scene(rng)
+    a = oracle_mod.denoise(G, Y, D=8, sigma=10.0, R=2)
+    b = oracle_mod.denoise(G[[2, 0, 3, 1]], Y, D=8, sigma=10.0, R=2)
+    np.testing.assert_allclose(a, b, rtol=1e-11, atol=1e-13)
+
+
+def test_p9_radiance_affine_equivariance(oracle_mod):
+    """The method is linear in X^T Y with the bias column: aY + b -> a I + b."""
+    rng = np.random.default_rng(22)
+    G, Y = _scene(rng)
+    a = oracle_mod.denoise(G, Y, D=8, sigma=10.0, R=2)
+    Y2 = (2.5 * Y.astype(np.float64) + 0.75)
+    b = oracle_mod.denoise(G, Y2.astype(np.float32), D=8, sigma=10.0, R=2)
+    Y2r = Y2.astype(np.float32).astype(np.float64)
+    ref = oracle_mod.denoise(G, Y2r.astype(np.float32), D=8, sigma=10.0, R=2)
+    np.testing.assert_allclose(b, ref, rtol=1e-13)
+    np.testing.assert_allclose(b, 2.5 * a + 0.75, rtol=1e-6, atol=1e-6)  # f32 rounding of Y2
+
+
+def test_p9_global_weight_scale_invariance(oracle_mod):
+    """Scaling all moments by a constant (unit-sum vs peak-1 Gaussian, R2) leaves A unchanged."""
+    rng = np.random.default_rng(23)
+    M = rng.normal(size=(5, 5))
+    M = M @ M.T + 5 * np.eye(5)
+    M[0, 0] = 7.0
+    N = rng.normal(size=(5, 3))
+    a = oracle_mod.solve_block(M, N)
+    b = oracle_mod.solve_block(M * 0.0137, N * 0.0137)
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-14)
+
+
+def test_p9_shift_invariance_iff_eps_mul_zero(oracle_mod):
+    """Adding a constant to one guide only moves mu_X; with eps_mul = 0 the output is
+    unchanged, with eps_mul > 0 (the diag(mu^2) and mu mu^T terms) it changes."""
+    rng = np.random.default_rng(24)
+    G, Y = _scene(rng)
+    G2 = G.copy()
+    G2[1] += np.float32(0.5)
+    a0 = oracle_mod.denoise(G, Y, D=8, sigma=10.0, R=2, eps_add=1e-5, eps_mul=0.0)
+    b0 = oracle_mod.denoise(G2, Y, D=8, sigma=10.0, R=2, eps_add=1e-5, eps_mul=0.0)
+    np.testing.assert_allclose(a0, b0, rtol=1e-5, atol=1e-6)
+    a1 = oracle_mod.denoise(G, Y, D=8, sigma=10.0, R=2, eps_add=1e-5, eps_mul=0.05)
+    b1 = oracle_mod.denoise(G2, Y, D=8, sigma=10.0, R=2, eps_add=1e-5, eps_mul=0.05)
+    assert np.abs(a1 - b1).max() > 1e-3
+
+
+def test_p9_scale_invariance_iff_eps_add_zero(oracle_mod):
+    """Scaling one guide: invariant with eps_add = 0 (any eps_mul); the eps_add I term breaks it."""
+    rng = np.random.default_rng(25)
+    G, Y = _scene(rng)
+    G2 = G.copy()
+    G2[2] *= np.float32(4.0)
+    a0 = oracle_mod.denoise(G, Y, D=8, sigma=10.0, R=2, eps_add=0.0, eps_mul=0.01)
+    b0 = oracle_mod.denoise(G2, Y, D=8, sigma=10.0, R=2, eps_add=0.0, eps_mul=0.01)
+    np.testing.assert_allclose(a0, b0, rtol=1e-8, atol=1e-9)
+    a1 = oracle_mod.denoise(G, Y, D=8, sigma=10.0, R=2, eps_add=0.05, eps_mul=0.01)
+    b1 = oracle_mod.denoise(G2, Y, D=8, sigma=10.0, R=2, eps_add=0.05, eps_mul=0.01)
+    assert np.abs(a1 - b1).max() > 1e-3
+
+
+def test_p9_constant_guide_noop_iff_eps_mul_zero(oracle_mod):
+    rng = np.random.default_rng(26)
+    G, Y = _scene(rng)
+    Gc = np.concatenate([G, np.full((1,) + G.shape[1:], 0.6, dtype=np.float32)])
+    a0 = oracle_mod.denoise(G, Y, D=8, sigma=10.0, R=2, eps_add=1e-4, eps_mul=0.0)
+    b0 = oracle_mod.denoise(Gc, Y, D=8, sigma=10.0, R=2, eps_add=1e-4, eps_mul=0.0)
+    np.testing.assert_allclose(a0, b0, rtol=1e-9, atol=1e-10)
+    a1 = oracle_mod.denoise(G, Y, D=8, sigma=10.0, R=2, eps_add=1e-4, eps_mul=0.2)
+    b1 = oracle_mod.denoise(Gc, Y, D=8, sigma=10.0, R=2, eps_add=1e-4, eps_mul=0.2)
+    assert np.abs(a1 - b1).max() > 1e-4
+
+
+# ---------------------------------------------------------------- P10: degenerate guides
+def test_p10_duplicated_and_flat_guides_stay_finite(oracle_mod):
+    """Rank-deficient moments (duplicated channel, exactly flat regions) must not give
+    NaNs with the default regularisation."""
+    from paper_2410_11625_b200 import synth
+
+    G, Y = synth.frame(96, 64, Q=8, seed=1234, duplicate_guide=True)
+    G = G.numpy()
+    G[:, :32, :] = G[:, :1, :1]  # a large exactly-flat region
+    out = oracle_mod.denoise(G, Y.numpy(), D=8, sigma=10.0)
+    assert np.isfinite(out).all()
+
+
+# ---------------------------------------------------------------- P11: apply weights
+def test_p11_apply_ramp_matches_golden(oracle_mod):
+    """Two blocks with bias 0 and 1 (zero slopes) give the cited ramp pattern."""
+    path = os.path.join(GOLDEN, "apply_ramp_D8.txt")
+    expect = np.loadtxt(path, comments="#")
+    A = np.zeros((1, 2, 2, 3))
+    A[0, 1, 0, :] = 1.0
+    G = np.zeros((1, 8, 16), dtype=np.float32)
+    out = oracle_mod.apply(A[None], G, 8)[0]
+    for c in range(3):
+        for y in range(8):
+            np.testing.assert_allclose(out[c, y], expect, rtol=0, atol=0)
+
+
+def test_p11_equal_models_give_plain_apply(oracle_mod):
+    rng = np.random.default_rng(31)
+    Q, H, W = 3, 13, 19
+    G = rand_planes(rng, Q, H, W)
+    A1 = rng.normal(size=(Q + 1, 3))
+    A = np.broadcast_to(A1, (2, 3, Q + 1, 3)).copy()
+    out = oracle_mod.apply(A[None], G, 8)[0]
+    Xt = np.concatenate([np.ones((1, H, W)), G.astype(np.float64)])
+    np.testing.assert_allclose(out, np.einsum("qhw,qc->chw", Xt, A1), rtol=1e-13, atol=1e-14)
+
+
+def test_p11_apply_matches_bruteforce_blend(oracle_mod):
+    rng = np.random.default_rng(32)
+    Q, H, W, D = 2, 21, 26, 4
+    G = rand_planes(rng, Q, H, W)
+    A = rng.normal(size=(6, 7, Q + 1, 3))
+    out = oracle_mod.apply(A[None], G, D)[0]
+    np.testing.assert_allclose(out, brute.apply_blend(A, G, D), rtol=1e-12, atol=1e-13)
+
+
+# ---------------------------------------------------------------- P12: upsample
+def test_p12_upsample_u1_is_denoise(oracle_mod):
+    rng = np.random.default_rng(41)
+    G, Y = _scene(rng)
+    a = oracle_mod.denoise(G, Y, D=4, sigma=10.0, R=3)
+    b = oracle_mod.denoise_upsample(G, Y, G, D_fit=4, U=1, sigma=10.0, R=3)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_p12_upsample_bruteforce(oracle_mod):
+    """Fit at low resolution with blocks of D_fit, blur std sigma/(D_fit U) blocks,
+    apply hi-res guides with D_out = D_fit U: brute force on pixels."""
+    rng = np.random.default_rng(42)
+    Q, H, W, D, U = 2, 10, 14, 2, 2
+    G = rand_planes(rng, Q, H, W)
+    Y = rand_planes(rng, 3, H, W)
+    Gh = rand_planes(rng, Q, H * U, W * U)
+    out = oracle_mod.denoise_upsample(G, Y, Gh, D_fit=D, U=U, sigma=6.0, R=2, eps_add=1e-3, eps_mul=1e-2)[0]
+    A = brute.fit_blocks(G, Y, D, 6.0, 2, 1e-3, 1e-2, U=U)
+    np.testing.assert_allclose(out, brute.apply_blend(A, Gh, D * U), rtol=1e-9, atol=1e-10)
+
+
+def test_p12_affine_field_exact_across_resolutions(oracle_mod):
+    rng = np.random.default_rng(43)
+    Q, H, W, U = 3, 16, 24, 2
+    Gh = rand_planes(rng, Q, H * U, W * U, -1, 1)
+    G = Gh[:, ::U, ::U].copy()
+    A_true = rng.normal(size=(Q + 1, 3))
+    Y = np.einsum("qhw,qc->chw", np.concatenate([np.ones((1, H, W)), G.astype(np.float64)]), A_true)
+    out = oracle_mod.denoise_upsample(G, Y.astype(np.float32), Gh, D_fit=4, U=U, sigma=16.0,
+                                      R=2, eps_add=0.0, eps_mul=0.0)[0]
+    ref = np.einsum("qhw,qc->chw", np.concatenate([np.ones((1, H * U, W * U)), Gh.astype(np.float64)]), A_true)
+    np.testing.assert_allclose(out, ref, atol=2e-5)
+
+
+# ---------------------------------------------------------------- argument errors
+def test_oracle_rejects_bad_arguments(oracle_mod):
+    G = np.zeros((1, 4, 4), dtype=np.float32)
+    Y = np.zeros((3, 4, 4), dtype=np.float32)
+    with pytest.raises(ValueError):
+        oracle_mod.fit(G, Y, D=4, sigma=-1.0, R=1)
+    with pytest.raises(ValueError):
+        oracle_mod.fit(G, Y, D=4, sigma=1.0, R=1, eps_mul=1.0)
