@@ -1,0 +1,546 @@
+#!/usr/bin/env python
+"""FLR fit+apply benchmark on B200 (contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl flr|reference]
+
+A "step" is one pass of the whole hot path -- block moments, moment blur, per-block
+solve, blended apply (a5 for --config c4) -- over one
+batch of `--frames-per-step` synthetic frames (default 1).  Inputs are resident in
+HBM before the timed region; the step rotates through a pool of distinct frames
+whose total size exceeds the 126 MB L2 (no cross-step L2 reuse).  The timed region
+is K steps replayed from CUDA graphs, bracketed by barrier + synchronize, timed with
+CUDA events on the launching stream; the max over ranks is reported.  Per-kernel
+durations (for the roofline of the dominant kernel) come from caller-owned CUDA
+events the library records between its launches inside the same timed region.
+
+Multi-GPU (torchrun, one rank per GPU): frames are independent, so every rank
+denoises its own frames (weak scaling); NCCL only carries the timing max and
+checksums after the timed region.
+
+--impl reference times the fp64 CPU oracle (oracle/flr_ref.c) on the host cores on
+a bounded sample of the same workload (a band of rows of the frame per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 1024 * 1024
+
+# BASELINE.json configs (SURVEY section 8(d) recipe)
+CONFIGS = {
+    "c1": dict(workload="C1 64x64 1spp Q=4 (albedo, normal.v, depth, AO), 8x8 blocks", W=64, H=64, Q=4,
+               block=8, upsample=1, sigma=10.0),
+    "c2": dict(workload="C2 1920x1080 1spp Q=8 (incl. 2 neural guide planes), 8x8 blocks", W=1920, H=1080,
+               Q=8, block=8, upsample=1, sigma=10.0),
+    "c3": dict(workload="C3 3840x2160 1spp Q=8, sigma=20 (larger window), 8x8 blocks", W=3840, H=2160, Q=8,
+               block=8, upsample=1, sigma=20.0),
+    "c4": dict(workload="C4 joint denoise+2x upsample: 960x540 1spp radiance, 1920x1080 guides, Q=8",
+               W=960, H=540, Q=8, block=4, upsample=2, sigma=10.0),
+    "c5": dict(workload="C5 batch of 1080p frames (Q=8, 8x8) frame-sharded over GPUs", W=1920, H=1080, Q=8,
+               block=8, upsample=1, sigma=10.0),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", choices=["flr", "reference"], default="flr")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--frames-per-step", type=int, default=None,
+                    help="frames per step per GPU (default 1; c5: 32)")
+    ap.add_argument("--pool", type=int, default=0, help="distinct frames rotated (0 = auto, > 2x L2)")
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step from Python")
+    ap.add_argument("--check", action="store_true", help="parity-check one frame against the oracle")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- helpers
+def out_pixels(cfg):
+    return cfg["W"] * cfg["upsample"] * cfg["H"] * cfg["upsample"]
+
+
+def min_bytes_per_frame(cfg):
+    """Algorithmic bytes: fp32 input planes read once + output written once."""
+    Q, W, H, U = cfg["Q"], cfg["W"], cfg["H"], cfg["upsample"]
+    lo = W * H
+    hi = lo * U * U
+    if U == 1:
+        return (Q + 3 + 3) * 4 * lo
+    return (Q + 3) * 4 * lo + Q * 4 * hi + 3 * 4 * hi
+
+
+KERNEL_BYTES = {
+    # algorithmic bytes per frame of each launch: the full-resolution planes it must read + write
+    "k_fit_moments": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
+    "k_apply_tile": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
+    "k_apply_px": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
+    "k_flr_fused": lambda c: min_bytes_per_frame(c),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel, config):
+    """dram__bytes_read+write per launch from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, index, period=0.005):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": getattr(nv, "nvmlClocksEventReasonGpuIdle", 0x1),
+            "applications_clocks_setting": getattr(nv, "nvmlClocksEventReasonApplicationsClocksSetting", 0x2),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sync_boost": getattr(nv, "nvmlClocksEventReasonSyncBoost", 0x10),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(cfg, budget_s, seed=777):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: bands of
+    full-width rows of the frame (multiples of the block size), until ~budget_s."""
+    import numpy as np
+
+    import oracle
+    from paper_2410_11625_b200 import synth
+
+    W, H, Q, D, U, sigma = cfg["W"], cfg["H"], cfg["Q"], cfg["block"], cfg["upsample"], cfg["sigma"]
+    R = math.ceil(2.0 * sigma / (D * U) - 1e-12)
+    band = min(H, max(D, (64 // D) * D))
+    if U == 1:
+        G, Y = synth.frame(W, band, Q=Q, seed=seed)
+        G, Y = G.numpy(), Y.numpy()
+        run = lambda: oracle.denoise(G, Y, D=D, sigma=sigma, R=R)  # noqa: E731
+    else:
+        g, y, gh = synth.upsample_pair(W, band, U=U, Q=Q, seed=seed)
+        g, y, gh = g.numpy(), y.numpy(), gh.numpy()
+        run = lambda: oracle.denoise_upsample(g, y, gh, D_fit=D, U=U, sigma=sigma, R=R)  # noqa: E731
+    px = W * band * U * U
+    run()  # warm (page-in, thread pool)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end or not times:
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    return {"value": px * len(times) / tot / 1e6, "unit": "Mpixel/s", "cores": oracle.num_threads(),
+            "kind": "oracle", "cpu": cpu_model(),
+            "sample": f"{len(times)} bands of {W}x{band} px{' (x%d upsample)' % U if U > 1 else ''} "
+                      f"of the {cfg['workload'].split(' ')[0]} workload, {tot:.1f} s",
+            "ms_per_frame_extrapolated": 1e3 * tot / len(times) * (cfg["H"] / band)}
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    from paper_2410_11625_b200 import synth
+
+    W, H, Q, D, U, sigma = cfg["W"], cfg["H"], cfg["Q"], cfg["block"], cfg["upsample"], cfg["sigma"]
+    R = math.ceil(2.0 * sigma / (D * U) - 1e-12)
+    # size each step so the whole run takes ~2 minutes at most
+    total_steps = args.steps + args.warmup
+    cal = oracle_sample(cfg, 1.0)
+    px_per_s = cal["value"] * 1e6
+    budget_px = 90.0 * px_per_s / max(1, total_steps)
+    rows = max(D, int(budget_px / (W * U * U) // D) * D)
+    rows = min(rows, H)
+    if U == 1:
+        G, Y = synth.frame(W, rows, Q=Q, seed=1000)
+        G, Y = G.numpy(), Y.numpy()
+        step = lambda: oracle.denoise(G, Y, D=D, sigma=sigma, R=R)  # noqa: E731
+    else:
+        g, y, gh = synth.upsample_pair(W, rows, U=U, Q=Q, seed=1000)
+        g, y, gh = g.numpy(), y.numpy(), gh.numpy()
+        step = lambda: oracle.denoise_upsample(g, y, gh, D_fit=D, U=U, sigma=sigma, R=R)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    px = W * rows * U * U
+    value = px * args.steps / dt / 1e6
+    line = {
+        "impl": "reference", "metric": "Mpixel/s (FLR fit+apply, 1spp, fp64 CPU oracle)", "value": value,
+        "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
+        "config": {"workload": cfg["workload"], "sample": f"{W}x{rows} band per step", "Q": Q, "block": D,
+                   "upsample": U, "sigma": sigma, "radius": R},
+        "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": f"{args.steps} steps of a {W}x{rows} band", "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- FLR arm
+def run_flr(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_11625_b200 as flr
+    from paper_2410_11625_b200 import synth
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    W, H, Q, D, U, sigma = cfg["W"], cfg["H"], cfg["Q"], cfg["block"], cfg["upsample"], cfg["sigma"]
+    F = args.frames_per_step or (32 if args.config == "c5" else 1)
+    frame_in_bytes = (Q + 3) * 4 * W * H + (Q * 4 * W * H * U * U if U > 1 else 0)
+    pool = args.pool or max(2, math.ceil(2.5 * L2_BYTES / (frame_in_bytes * F)))
+    R = flr.effective_radius(block=D, upsample=U, sigma=sigma)
+
+    # ---- inputs resident in HBM (global frame index -> seed; ranks draw disjoint frames)
+    base_seed = 1000 + rank * pool * F
+    gl, yl, gh = [], [], []
+    for i in range(pool):
+        if U == 1:
+            g, y = synth.batch(F, W, H, Q=Q, seed0=base_seed + i * F, device=dev)
+            gl.append(g)
+            yl.append(y)
+        else:
+            trip = [synth.upsample_pair(W, H, U=U, Q=Q, seed=base_seed + i * F + j, device=dev) for j in range(F)]
+            gl.append(torch.stack([t[0] for t in trip]).contiguous())
+            yl.append(torch.stack([t[1] for t in trip]).contiguous())
+            gh.append(torch.stack([t[2] for t in trip]).contiguous())
+    torch.cuda.synchronize()
+    den = flr.Denoiser(F, Q, W, H, device=dev, block=D, upsample=U, sigma=sigma, variant=args.variant)
+    outs = [torch.empty_like(den.out) for _ in range(2)]
+
+    def call(i, trace=None):
+        k = i % pool
+        return den(gl[k], yl[k], gh[k] if U > 1 else None, out=outs[i % 2], trace=trace)
+
+    # ---- launch count + optional parity check
+    call(0)
+    launches_per_step = flr.last_launch_count()
+    kernel_names = flr.last_launch_names()
+    torch.cuda.synchronize()
+    check = None
+    if args.check and rank == 0:
+        import oracle
+        from tests.parity import parity_report
+
+        o = call(0).cpu().numpy()
+        g0 = gl[0].cpu().numpy()
+        y0 = yl[0].cpu().numpy()
+        if U == 1:
+            ref = oracle.denoise(g0, y0, D=D, sigma=sigma, R=R)
+        else:
+            ref = oracle.denoise_upsample(g0, y0, gh[0].cpu().numpy(), D_fit=D, U=U, sigma=sigma, R=R)
+        check = parity_report(o, ref)
+
+    stream = torch.cuda.current_stream(dev)
+    n_ev = launches_per_step + 1
+
+    def make_events(n):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        for e in evs:
+            e.record(stream)
+        return evs
+
+    # per-step traces for one pool rotation (reused every replay)
+    traces = [flr.EventTrace.from_events(make_events(n_ev)) for _ in range(pool)]
+
+    # ---- warm-up (untimed)
+    for i in range(max(3, args.warmup)):
+        call(i)
+    torch.cuda.synchronize()
+
+    # ---- CUDA graphs: one for a full pool rotation (traced), one for the remainder
+    K = args.steps
+    use_graph = not args.no_graph
+    graphs = {}
+    if use_graph:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            for i in range(pool):  # warm allocations on the capture stream
+                call(i)
+        torch.cuda.synchronize()
+
+        def capture(nsteps):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for i in range(nsteps):
+                    call(i, trace=traces[i])
+            return g
+
+        reps, rem = divmod(K, pool)
+        if reps:
+            graphs["full"] = capture(pool)
+        if rem:
+            graphs["rem"] = capture(rem)
+        torch.cuda.synchronize()
+
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_stop = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else local_rank)
+    with sampler:
+        time.sleep(0.02)
+        t_start.record(stream)
+        if use_graph:
+            reps, rem = divmod(K, pool)
+            for _ in range(reps):
+                graphs["full"].replay()
+            if rem:
+                graphs["rem"].replay()
+        else:
+            for i in range(K):
+                call(i, trace=traces[i % pool])
+        t_stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_stop)
+    clocks = sampler.summary()
+
+    # per-launch durations from the last recorded pool rotation
+    names = kernel_names
+    per_kernel = {n: [] for n in names}
+    used = traces if (not use_graph or K >= pool) else traces[:K]
+    for tr in used:
+        evs = tr._keep[1]
+        for j in range(min(len(names), tr.recorded - 1 if tr.recorded else len(evs) - 1)):
+            per_kernel[names[j]].append(evs[j].elapsed_time(evs[j + 1]))
+    avg_ms = {n: (sum(v) / len(v) if v else None) for n, v in per_kernel.items()}
+
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # ---- end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
+    E = max(1, args.e2e_steps)
+    e2e = None
+    if E:
+        hp = min(pool, 2)
+        h_g = [gl[k].cpu().pin_memory() for k in range(hp)]
+        h_y = [yl[k].cpu().pin_memory() for k in range(hp)]
+        h_gh = [gh[k].cpu().pin_memory() for k in range(hp)] if U > 1 else None
+        h_out = den.out.cpu().pin_memory()
+        d_g, d_y = torch.empty_like(gl[0]), torch.empty_like(yl[0])
+        d_gh = torch.empty_like(gh[0]) if U > 1 else None
+        h2d = sum(t.numel() * 4 for t in (d_g, d_y)) + (d_gh.numel() * 4 if U > 1 else 0)
+        d2h = h_out.numel() * 4
+
+        def e2e_step(i):
+            k = i % hp
+            d_g.copy_(h_g[k], non_blocking=True)
+            d_y.copy_(h_y[k], non_blocking=True)
+            if U > 1:
+                d_gh.copy_(h_gh[k], non_blocking=True)
+            o = den(d_g, d_y, d_gh)
+            h_out.copy_(o, non_blocking=True)
+
+        for i in range(3):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(E):
+            e2e_step(i)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms.item())
+        e2e = {"value": world * E * F * out_pixels(cfg) / (e_ms * 1e-3) / 1e6, "unit": "Mpixel/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / E, "steps": E}
+
+    # ---- checksums of one output per rank, gathered over NCCL (the only collective)
+    o = call(0)
+    torch.cuda.synchronize()
+    cs = torch.tensor([float(o.double().sum()), float(o.double().abs().max()),
+                       float(torch.isfinite(o).all())], dtype=torch.float64, device=dev)
+    if world > 1:
+        allcs = [torch.empty_like(cs) for _ in range(world)]
+        dist.all_gather(allcs, cs)
+    else:
+        allcs = [cs]
+
+    if rank != 0:
+        return
+    peak, peak_src = load_peaks()
+    frames_total = world * K * F
+    px_total = frames_total * out_pixels(cfg)
+    value = px_total / (ms_max * 1e-3) / 1e6
+    # dominant kernel (largest share of the step) and its own algorithmic bytes
+    known = {n: t for n, t in avg_ms.items() if t}
+    dom = max(known, key=known.get) if known else None
+    roof = None
+    if dom:
+        bytes_fn = KERNEL_BYTES.get(dom)
+        alg = bytes_fn(cfg) * F if bytes_fn else None
+        if alg is not None:
+            ach = alg / (known[dom] * 1e-3) / 1e9
+            roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": ncu_traffic(dom, args.config),
+                    "algorithmic_bytes_per_launch": alg, "avg_launch_us": known[dom] * 1e3,
+                    "peak_source": peak_src}
+        else:
+            roof = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": None, "frac": None,
+                    "traffic": None, "avg_launch_us": known[dom] * 1e3}
+    step_ms = ms_max / K
+    step_bytes = min_bytes_per_frame(cfg) * F
+    step_roof = {"min_bytes_per_step": step_bytes, "achieved": step_bytes / (step_ms * 1e-3) / 1e9,
+                 "peak": peak, "unit": "GB/s", "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak}
+    cpu_base = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu_base = oracle_sample(cfg, args.cpu_seconds)
+    line = {
+        "metric": "Mpixel/s (FLR fit+apply, 1spp) and ms per frame; % of HBM BW",
+        "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": step_ms, "ms_per_frame": step_ms / F, "frames_per_s": frames_total / (ms_max * 1e-3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded procedural Lambertian scenes, rasterised guides, 1spp noise)",
+        "config": {"workload": cfg["workload"], "W": W, "H": H, "Q": Q, "block": D, "upsample": U, "sigma": sigma,
+                   "radius": R, "eps_add": 1e-5, "eps_mul": 1e-4, "frames_per_step": F, "global_batch": world * F,
+                   "pool_frames": pool, "l2": f"rotating pool of {pool} distinct steps "
+                   f"({pool * F * frame_in_bytes / 1e6:.0f} MB > 126 MB L2)", "graphs": use_graph,
+                   "parallelism": f"frame-sharded dp{world}", "variant": args.variant,
+                   "numerics": "fp32 streams, fp64 block blur+solve"},
+        "roofline": roof, "step_roofline": step_roof,
+        "kernel_us": {n: (t * 1e3 if t else None) for n, t in avg_ms.items()},
+        "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": launches_per_step * K,
+        "clocks": clocks,
+        "checksums": [[float(v) for v in c.tolist()] for c in allcs],
+        "paper_context": {"rtx2080ti_ms_per_1080p_frame": 0.636, "source": "P:429 (Table 1)"},
+    }
+    if check is not None:
+        line["parity"] = check
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = dict(CONFIGS[args.config])
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            sys.exit(f"--gpus {args.gpus} needs torchrun --nproc-per-node {args.gpus}")
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_flr(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,133 @@
+// flr_solve.cuh -- the appendix's normalised, regularised per-block solve
+// as one fp64 in-register device function, shared by every kernel schedule.
+//
+//   n = M_00, mu_X = u_X / n, mu_Y = N_0 / n
+//   W^ = S/n + eps_mul diag(mu^2) + eps_add I - (1 - eps_mul) mu mu^T (R7, R8)
+//   sigma^ = sqrt(max(diag W^, 1e-300))                            (R11)
+//   C^_ij = W^_ij / (sigma^_i sigma^_j)
+//   B^_ic = (XY_ic / n - mu_i mu_Y,c) / sigma^_i                   (R9)
+//   A^ = (C^ + eps_add I)^-1 B^
+//   raw model (R6): A[1+j][c] = A^[j][c] / sigma^_j,  A[0][c] = mu_Y,c - sum_j mu_j A[1+j][c]
+//
+// (C^ + eps_add I) is symmetric positive definite for eps_add > 0 (R13), so the
+// solve is a Cholesky factorisation + two triangular solves instead of the
+// paper's recursive block inverse: the solution is unique, so any
+// exact solver returns it up to rounding.
+#pragma once
+#include <type_traits>
+
+#include "flr_common.cuh"
+
+namespace flr {
+
+// compile-time loop: f(integral_constant<int, 0>) ... f(integral_constant<int, N-1>), so every
+// array index below is a constant and the factor stays in registers
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f)
+{
+    if constexpr (N > 0) {
+        static_for<N - 1>(f);
+        f(std::integral_constant<int, N - 1>{});
+    }
+}
+
+// `m(k)` returns the blurred fp64 moment component k (layout of flr_common.cuh).
+// Writes 3(Q+1) floats to `out` (row 0 = bias).
+template <int Q, class MomentFn>
+__device__ __forceinline__ void solve_block(MomentFn&& m, double eps_add, double eps_mul, float* out)
+{
+    using Dm = Dims<Q>;
+    const double n = m(Dm::C_N);
+    const double inv_n = 1.0 / n;
+    double mu[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) mu[j] = m(Dm::C_U + j) * inv_n;
+    double Wh[Dm::NS];
+    const double om = 1.0 - eps_mul;
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+        for (int j = i; j < Q; ++j) {
+            double w = fma(m(Dm::s_idx(i, j)), inv_n, -om * mu[i] * mu[j]);
+            if (i == j) w += fma(eps_mul * mu[i], mu[i], eps_add);
+            Wh[Dm::s_idx(i, j) - Dm::C_S] = w;
+        }
+    double isig[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) isig[i] = 1.0 / sqrt(fmax(Wh[Dm::s_idx(i, i) - Dm::C_S], 1e-300));
+    double muY[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) muY[c] = m(Dm::C_Y + c) * inv_n;
+    double B[Q][3];
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) B[i][c] = fma(m(Dm::C_XY + i * 3 + c), inv_n, -mu[i] * muY[c]) * isig[i];
+    // C^ + eps I in place (upper triangle)
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+        for (int j = i; j < Q; ++j) {
+            const int k = Dm::s_idx(i, j) - Dm::C_S;
+            Wh[k] = Wh[k] * isig[i] * isig[j] + (i == j ? eps_add : 0.0);
+        }
+    // Cholesky C = R^T R (R upper, in place)
+    double rinv[Q];
+    static_for<Q>([&](auto K) {
+        constexpr int k = decltype(K)::value;
+        double dkk = Wh[Dm::s_idx(k, k) - Dm::C_S];
+        static_for<k>([&](auto PP) {
+            constexpr int p = decltype(PP)::value;
+            const double r = Wh[Dm::s_idx(p, k) - Dm::C_S];
+            dkk = fma(-r, r, dkk);
+        });
+        rinv[k] = 1.0 / sqrt(dkk);
+        static_for<Q - k - 1>([&](auto JJ) {
+            constexpr int j = k + 1 + decltype(JJ)::value;
+            double v = Wh[Dm::s_idx(k, j) - Dm::C_S];
+            static_for<k>([&](auto PP) {
+                constexpr int p = decltype(PP)::value;
+                v = fma(-Wh[Dm::s_idx(p, k) - Dm::C_S], Wh[Dm::s_idx(p, j) - Dm::C_S], v);
+            });
+            Wh[Dm::s_idx(k, j) - Dm::C_S] = v * rinv[k];
+        });
+    });
+    // R^T z = B, then R A^ = z
+    static_for<Q>([&](auto K) {
+        constexpr int k = decltype(K)::value;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double v = B[k][c];
+            static_for<k>([&](auto PP) {
+                constexpr int p = decltype(PP)::value;
+                v = fma(-Wh[Dm::s_idx(p, k) - Dm::C_S], B[p][c], v);
+            });
+            B[k][c] = v * rinv[k];
+        }
+    });
+    static_for<Q>([&](auto KK) {
+        constexpr int k = Q - 1 - decltype(KK)::value;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double v = B[k][c];
+            static_for<Q - 1 - k>([&](auto PP) {
+                constexpr int p = k + 1 + decltype(PP)::value;
+                v = fma(-Wh[Dm::s_idx(k, p) - Dm::C_S], B[p][c], v);
+            });
+            B[k][c] = v * rinv[k];
+        }
+    });
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double bias = muY[c];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+            const double a = B[j][c] * isig[j];
+            out[(1 + j) * 3 + c] = (float)a;
+            bias = fma(-mu[j], a, bias);
+        }
+        out[c] = (float)bias;
+    }
+}
+
+}  // namespace flr

@@ -1,0 +1,206 @@
+"""GPU <-> oracle parity (-m gpu): the CUDA path through the C ABI vs oracle/flr_ref.c.
+
+Every case draws seeded synthetic inputs on the CPU (paper_2410_11625_b200.synth),
+runs the oracle on them and the CUDA path on a device copy of the same tensors,
+and requires zero elementwise violations of |gpu - ref| <= 1e-5 + 1e-4 |ref|.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.parity import assert_parity, parity_report
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def flr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2410_11625_b200 as m
+
+    m.lib()
+    return m
+
+
+def _inputs(W, H, Q, seed, **kw):
+    from paper_2410_11625_b200 import synth
+
+    G, Y = synth.frame(W, H, Q=Q, seed=seed, **kw)
+    return G, Y
+
+
+def _run_denoise(flr, oracle_mod, G, Y, **p):
+    out = flr.denoise(G.cuda(), Y.cuda(), **p)
+    torch.cuda.synchronize()
+    ref = oracle_mod.denoise(G.numpy(), Y.numpy(), D=p.get("block", 8), sigma=p.get("sigma", 10.0),
+                             R=flr.effective_radius(block=p.get("block", 8), sigma=p.get("sigma", 10.0),
+                                                    radius=p.get("radius", 0)),
+                             eps_add=p.get("eps_add", 1e-5), eps_mul=p.get("eps_mul", 1e-4))
+    return out.cpu().numpy(), ref
+
+
+# ------------------------------------------------------------------ BASELINE configs
+def test_c1_64x64_q4(flr, oracle_mod):
+    G, Y = _inputs(64, 64, 4, 1000)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y)
+    assert_parity(out, ref[None] if ref.ndim == 3 else ref, "C1")
+
+
+def test_c2_1080p_q8(flr, oracle_mod):
+    G, Y = _inputs(1920, 1080, 8, 1001)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y)
+    rep = assert_parity(out, ref, "C2")
+    print("C2 parity", rep)
+
+
+def test_c3_4k_q8_sigma20(flr, oracle_mod):
+    G, Y = _inputs(3840, 2160, 8, 1002)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y, sigma=20.0)
+    rep = assert_parity(out, ref, "C3")
+    print("C3 parity", rep)
+
+
+def test_c4_joint_upsample(flr, oracle_mod):
+    from paper_2410_11625_b200 import synth
+
+    g_lo, y_lo, g_hi = synth.upsample_pair(960, 540, U=2, Q=8, seed=1003)
+    out = flr.denoise_upsample(g_lo.cuda(), y_lo.cuda(), g_hi.cuda(), block=4, upsample=2)
+    torch.cuda.synchronize()
+    R = flr.effective_radius(block=4, upsample=2)
+    ref = oracle_mod.denoise_upsample(g_lo.numpy(), y_lo.numpy(), g_hi.numpy(), D_fit=4, U=2, sigma=10.0, R=R)
+    rep = assert_parity(out.cpu().numpy(), ref, "C4")
+    print("C4 parity", rep)
+
+
+def test_c5_batch_of_frames(flr, oracle_mod):
+    """A batch of independent frames in one call equals per-frame oracle results."""
+    from paper_2410_11625_b200 import synth
+
+    G, Y = synth.batch(3, 320, 184, Q=8, seed0=2000)
+    out = flr.denoise(G.cuda(), Y.cuda())
+    torch.cuda.synchronize()
+    ref = oracle_mod.denoise(G.numpy(), Y.numpy(), D=8, sigma=10.0, R=3)
+    assert_parity(out.cpu().numpy(), ref, "C5 batch")
+
+
+# ------------------------------------------------------------------ sweeps
+@pytest.mark.parametrize("Q", [1, 2, 4, 8, 11, 15])
+def test_sweep_q(flr, oracle_mod, Q):
+    G, Y = _inputs(136, 72, Q, 3000 + Q)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y)
+    assert_parity(out, ref, f"Q={Q}")
+
+
+@pytest.mark.parametrize("block", [1, 2, 4, 8, 16])
+def test_sweep_block(flr, oracle_mod, block):
+    G, Y = _inputs(96, 80, 4, 3100 + block)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y, block=block, sigma=max(2.0, 1.25 * block))
+    assert_parity(out, ref, f"block={block}")
+
+
+@pytest.mark.parametrize("W,H", [(37, 23), (65, 9), (8 * 13 + 1, 8 * 5 + 1), (1, 1), (3, 7), (130, 66)])
+def test_odd_sizes(flr, oracle_mod, W, H):
+    """Partial blocks, scalar tails (W % 4 != 0), clamped bilinear interpolation."""
+    G, Y = _inputs(W, H, 8, 3200 + W)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y)
+    assert_parity(out, ref, f"{W}x{H}")
+
+
+@pytest.mark.parametrize("radius", [1, 3, 5, 8, 10])
+def test_sweep_radius(flr, oracle_mod, radius):
+    G, Y = _inputs(128, 96, 8, 3300 + radius)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y, radius=radius)
+    assert_parity(out, ref, f"R={radius}")
+
+
+@pytest.mark.parametrize("eps_add,eps_mul", [(1e-5, 1e-4), (1e-5, 0.0), (0.0, 1e-4), (1e-4, 1e-5)])
+def test_sweep_eps(flr, oracle_mod, eps_add, eps_mul):
+    from paper_2410_11625_b200 import synth
+
+    # eps_add = 0 needs non-degenerate windows (R11): random guides
+    if eps_add == 0.0:
+        G = synth.uniform_noise((4, 64, 96), seed=3400)
+        _, Y = _inputs(96, 64, 4, 3401)
+    else:
+        G, Y = _inputs(96, 64, 8, 3402)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y, eps_add=eps_add, eps_mul=eps_mul)
+    assert_parity(out, ref, f"eps=({eps_add},{eps_mul})")
+
+
+@pytest.mark.parametrize("block,U", [(4, 2), (8, 2), (2, 4), (4, 4), (8, 3), (1, 2)])
+def test_sweep_upsample(flr, oracle_mod, block, U):
+    from paper_2410_11625_b200 import synth
+
+    g_lo, y_lo, g_hi = synth.upsample_pair(60, 34, U=U, Q=8, seed=3500 + U * 10 + block)
+    out = flr.denoise_upsample(g_lo.cuda(), y_lo.cuda(), g_hi.cuda(), block=block, upsample=U)
+    torch.cuda.synchronize()
+    R = flr.effective_radius(block=block, upsample=U)
+    ref = oracle_mod.denoise_upsample(g_lo.numpy(), y_lo.numpy(), g_hi.numpy(), D_fit=block, U=U,
+                                      sigma=10.0, R=R)
+    assert_parity(out.cpu().numpy(), ref, f"upsample D={block} U={U}")
+
+
+# ------------------------------------------------------------------ stress inputs (H1)
+def test_stress_duplicate_guide_and_flat_region(flr, oracle_mod):
+    G, Y = _inputs(512, 288, 8, 3600, duplicate_guide=True)
+    G = G.clone()
+    G[:, :96, :] = G[:, :1, :1]  # exactly flat guides over a large area
+    out, ref = _run_denoise(flr, oracle_mod, G, Y)
+    rep = assert_parity(out, ref, "stress")
+    print("stress parity", rep)
+
+
+def test_stress_fireflies_and_crowded_depth(flr, oracle_mod):
+    G, Y = _inputs(400, 240, 8, 3601)
+    G = G.clone()
+    Y = Y.clone()
+    G[4] = 0.999 + 0.001 * G[4]  # depth crowded into [0.999, 1]
+    Y[:, ::7, ::5] *= 50.0        # extra fireflies
+    out, ref = _run_denoise(flr, oracle_mod, G, Y)
+    assert_parity(out, ref, "fireflies")
+
+
+# ------------------------------------------------------------------ stage isolation
+def test_fit_models_through_oracle_apply(flr, oracle_mod):
+    """GPU fit, oracle apply (fp64): isolates the fit's error from the apply's."""
+    G, Y = _inputs(256, 160, 8, 3700)
+    models = flr.fit(G.cuda(), Y.cuda())
+    torch.cuda.synchronize()
+    out = oracle_mod.apply(models.cpu().numpy().astype(np.float64), G.numpy(), 8)
+    ref = oracle_mod.denoise(G.numpy(), Y.numpy(), D=8, sigma=10.0, R=3)
+    assert_parity(out, ref, "fit-only")
+
+
+def test_apply_on_oracle_models(flr, oracle_mod):
+    """Oracle fit, GPU apply: isolates the apply (models rounded to fp32 on both sides)."""
+    G, Y = _inputs(200, 120, 8, 3701)
+    A = oracle_mod.fit(G.numpy(), Y.numpy(), D=8, sigma=10.0, R=3).astype(np.float32)
+    out = flr.apply(torch.from_numpy(A).cuda(), G.cuda(), 8)
+    torch.cuda.synchronize()
+    ref = oracle_mod.apply(A.astype(np.float64), G.numpy(), 8)
+    assert_parity(out.cpu().numpy(), ref, "apply-only")
+
+
+# ------------------------------------------------------------------ determinism / errors
+def test_deterministic(flr):
+    G, Y = _inputs(320, 200, 8, 3800)
+    a = flr.denoise(G.cuda(), Y.cuda())
+    b = flr.denoise(G.cuda(), Y.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_errors_raise(flr):
+    G, Y = _inputs(64, 64, 8, 3900)
+    with pytest.raises(ValueError):
+        flr.denoise(G, Y)  # CPU tensors: no fallback
+    with pytest.raises(flr.FLRError):
+        flr.denoise(G.cuda(), Y.cuda(), block=3)
+    with pytest.raises(flr.FLRError):
+        flr.denoise(G.cuda(), Y.cuda(), sigma=-1.0)
+
+
+def test_parity_report_helper():
+    r = parity_report(np.array([1.0, 2.0]), np.array([1.0, 2.0001]))
+    assert r["violations"] == 0
