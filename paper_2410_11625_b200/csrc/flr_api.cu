@@ -52,10 +52,11 @@ Layout layout(int n, int Q, int Bx, int By)
     size_t off = 0;
     L.raw = off;
     off += align256(nb * kraw_of(Q) * sizeof(float));
+    const size_t nbp = (size_t)n * mom_pitch(Bx) * By;  // pitched moment rows (TMA)
     L.mom = off;
-    off += align256(nb * km_of(Q) * sizeof(double));
+    off += align256(nbp * km_of(Q) * sizeof(double));
     L.hb = off;
-    off += align256(nb * km_of(Q) * sizeof(double));
+    off += align256(nbp * km_of(Q) * sizeof(double));
     L.models = off;
     off += align256(nb * mstride_of(Q) * sizeof(float));
     L.total = off;

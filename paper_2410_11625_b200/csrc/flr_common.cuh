@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace flr {
 
 constexpr int kMaxQ = 15;
@@ -41,6 +43,17 @@ struct Dims {
 inline int km_of(int Q) { return 1 + Q + Q * (Q + 1) / 2 + 3 + 3 * Q; }
 inline int kraw_of(int Q) { return km_of(Q) + Q; }
 inline int mstride_of(int Q) { return ((3 * (Q + 1) + 3) / 4) * 4; }
+
+// compile-time loop: f(integral_constant<int, 0>) ... f(integral_constant<int, N-1>), so every
+// array index below is a constant and the factor stays in registers
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f)
+{
+    if constexpr (N > 0) {
+        static_for<N - 1>(f);
+        f(std::integral_constant<int, N - 1>{});
+    }
+}
 
 struct Taps {
     double g[2 * kMaxR + 1];  // g[R + i] = exp(-i^2 / (2 s^2))

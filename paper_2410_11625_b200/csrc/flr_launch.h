@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "flr_common.cuh"
 
 namespace flr {
@@ -11,6 +14,37 @@ namespace flr {
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 inline bool aligned(const void* ptr, size_t a) { return ((uintptr_t)ptr % a) == 0; }
 inline bool vec_ok(const void* ptr, int W) { return aligned(ptr, 16) && (W % 4) == 0; }
+
+// 3-D TMA tensor map over `planes` planes of W x H elements (row stride `pitch` elements):
+// box {bx, by, bz}.  Requires pitch * esize % 16 == 0 and a 16-byte aligned base.
+// Out-of-range box elements read as 0.
+inline bool make_tmap_3d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int W, int H,
+                         int pitch, int planes, int bx, int by, int bz)
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)pitch * esize, (cuuint64_t)pitch * H * esize};
+    const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// fp32 planes [planes][H][W], box {bx, 1, bz}
+inline bool make_tmap_planes(CUtensorMap* m, const float* base, int W, int H, int planes, int bx, int bz)
+{
+    return make_tmap_3d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, W, planes, bx, 1, bz);
+}
+// moment-field row pitch (elements): even, so rows are 16-byte aligned for TMA
+inline int mom_pitch(int Bx) { return (Bx + 1) & ~1; }
 
 // Per-call launch context: the caller's stream, a launch counter, and an optional
 // caller-owned event trace (events[i] is recorded right before launch i and one

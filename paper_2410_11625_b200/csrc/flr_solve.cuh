@@ -14,22 +14,9 @@
 // paper's recursive block inverse: the solution is unique, so any
 // exact solver returns it up to rounding.
 #pragma once
-#include <type_traits>
-
 #include "flr_common.cuh"
 
 namespace flr {
-
-// compile-time loop: f(integral_constant<int, 0>) ... f(integral_constant<int, N-1>), so every
-// array index below is a constant and the factor stays in registers
-template <int N, class F>
-__device__ __forceinline__ void static_for(F&& f)
-{
-    if constexpr (N > 0) {
-        static_for<N - 1>(f);
-        f(std::integral_constant<int, N - 1>{});
-    }
-}
 
 // `m(k)` returns the blurred fp64 moment component k (layout of flr_common.cuh).
 // Writes 3(Q+1) floats to `out` (row 0 = bias).

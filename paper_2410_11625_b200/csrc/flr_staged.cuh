@@ -91,49 +91,51 @@ __global__ void __launch_bounds__(128) k_moments_small(int W, int H, int Bx, int
 //   XY_jc = XY'_jc + c_j Y_c.   One thread per block; SoA fp64 output [f][KM][By][Bx].
 // ---------------------------------------------------------------------------
 template <int Q>
-__global__ void __launch_bounds__(128) k_unshift(int nblk_frame, const float* __restrict__ raw,
+__global__ void __launch_bounds__(128) k_unshift(int Bx, int Bxp, int By, const float* __restrict__ raw,
                                                  double* __restrict__ mom)
 {
     using Dm = Dims<Q>;
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     const int f = blockIdx.y;
+    const int nblk_frame = Bx * By;
     if (b >= nblk_frame) return;
     const size_t cs = (size_t)nblk_frame;
     const float* in = raw + (size_t)f * Dm::KRAW * cs + b;
-    double* out = mom + (size_t)f * Dm::KM * cs + b;
+    const size_t co = (size_t)By * Bxp;  // output component stride (pitched rows)
+    double* out = mom + (size_t)f * Dm::KM * co + (size_t)(b / Bx) * Bxp + (b % Bx);
     const double n = (double)in[0];
     double c[Q], u[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
-        c[j] = (double)in[(size_t)(Dm::C_SH + j) * cs];
-        u[j] = (double)in[(size_t)(Dm::C_U + j) * cs];
+        c[j] = (double)in[(size_t)(Dm::C_SH + j) * co];
+        u[j] = (double)in[(size_t)(Dm::C_U + j) * co];
     }
     out[0] = n;
 #pragma unroll
-    for (int j = 0; j < Q; ++j) out[(size_t)(Dm::C_U + j) * cs] = fma(n, c[j], u[j]);
+    for (int j = 0; j < Q; ++j) out[(size_t)(Dm::C_U + j) * co] = fma(n, c[j], u[j]);
 #pragma unroll
     for (int i = 0; i < Q; ++i)
 #pragma unroll
         for (int j = i; j < Q; ++j) {
             const int k = Dm::s_idx(i, j);
-            double s = (double)in[(size_t)k * cs];
+            double s = (double)in[(size_t)k * co];
             s = fma(c[i], u[j], s);
             s = fma(c[j], u[i], s);
             s = fma(n * c[i], c[j], s);
-            out[(size_t)k * cs] = s;
+            out[(size_t)k * co] = s;
         }
     double yc[3];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
-        yc[cc] = (double)in[(size_t)(Dm::C_Y + cc) * cs];
-        out[(size_t)(Dm::C_Y + cc) * cs] = yc[cc];
+        yc[cc] = (double)in[(size_t)(Dm::C_Y + cc) * co];
+        out[(size_t)(Dm::C_Y + cc) * co] = yc[cc];
     }
 #pragma unroll
     for (int j = 0; j < Q; ++j)
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) {
             const int k = Dm::C_XY + j * 3 + cc;
-            out[(size_t)k * cs] = fma(c[j], yc[cc], (double)in[(size_t)k * cs]);
+            out[(size_t)k * co] = fma(c[j], yc[cc], (double)in[(size_t)k * co]);
         }
 }
 
@@ -142,17 +144,17 @@ __global__ void __launch_bounds__(128) k_unshift(int nblk_frame, const float* __
 // (P:299-309), fp64, zero padding (R3).  One thread per element
 // of [f][KM][By][Bx]; `rows` = n*KM*By.
 // ---------------------------------------------------------------------------
-static __global__ void __launch_bounds__(256) k_hblur(int Bx, size_t rows, const double* __restrict__ in,
+static __global__ void __launch_bounds__(256) k_hblur(int Bx, int Bxp, size_t rows, const double* __restrict__ in,
                                                double* __restrict__ out, const __grid_constant__ Taps t)
 {
     const int bx = blockIdx.x * blockDim.x + threadIdx.x;
     const size_t row = blockIdx.y + (size_t)blockIdx.z * gridDim.y;
     if (bx >= Bx || row >= rows) return;
-    const double* src = in + row * Bx;
+    const double* src = in + row * Bxp;
     double acc = 0.0;
     const int lo = max(-t.R, -bx), hi = min(t.R, Bx - 1 - bx);
     for (int d = lo; d <= hi; ++d) acc = fma(t.g[t.R + d], __ldg(src + bx + d), acc);
-    out[row * Bx + bx] = acc;
+    out[row * Bxp + bx] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -165,7 +167,7 @@ static __global__ void __launch_bounds__(256) k_hblur(int Bx, size_t rows, const
 // per block ([f][By][Bx][mstride]).
 // ---------------------------------------------------------------------------
 template <int Q>
-__global__ void __launch_bounds__(128) k_vblur_solve(int Bx, int By, const double* __restrict__ hb,
+__global__ void __launch_bounds__(128) k_vblur_solve(int Bx, int Bxp, int By, const double* __restrict__ hb,
                                                      float* __restrict__ models, int mstride,
                                                      double eps_add, double eps_mul,
                                                      const __grid_constant__ Taps t)
@@ -175,13 +177,13 @@ __global__ void __launch_bounds__(128) k_vblur_solve(int Bx, int By, const doubl
     const int by = blockIdx.y * blockDim.y + threadIdx.y;
     const int f = blockIdx.z;
     if (bx >= Bx || by >= By) return;
-    const size_t cs = (size_t)Bx * By;
+    const size_t cs = (size_t)Bxp * By;
     const double* base = hb + (size_t)f * Dm::KM * cs + bx;
     const int lo = max(-t.R, -by), hi = min(t.R, By - 1 - by);
     auto vb = [&](int k) -> double {
         const double* src = base + (size_t)k * cs;
         double acc = 0.0;
-        for (int d = lo; d <= hi; ++d) acc = fma(t.g[t.R + d], __ldg(src + (size_t)(by + d) * Bx), acc);
+        for (int d = lo; d <= hi; ++d) acc = fma(t.g[t.R + d], __ldg(src + (size_t)(by + d) * Bxp), acc);
         return acc;
     };
 

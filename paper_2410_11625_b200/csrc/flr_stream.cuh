@@ -1,0 +1,392 @@
+// flr_stream.cuh -- warp-granular streaming of full-resolution planes through a
+// per-warp shared-memory ring filled by the TMA engine.
+//
+// Every stream warp owns a ring of S stages.  A stage holds one pixel row of a
+// 128-pixel segment of every plane an item needs, fetched by ONE 3-D TMA tensor
+// load per tensor (box 128 x 1 x planes; out-of-image pixels arrive as zeros)
+// that completes on the stage's mbarrier.  Lane 0 of the warp keeps the producer
+// cursor and refills a stage as soon as the warp has read it, so S rows stay in
+// flight per warp.  Two item kinds:
+//   FIT: one block row x 128 fit pixels -> fp64
+//         moments of 128/D blocks: fp32 accumulation about the per-block shift c
+//         (design rule H1) with packed FFMA2 pairs, exact fp64 un-shift.
+//   APPLY: 8 output rows x 128 output pixels,
+//         I = x~ A_blend, with the two bracketing rows of block models delivered
+//         as one extra (bulk-copy) stage.
+#pragma once
+#include <cuda.h>
+
+#include "flr_common.cuh"
+#include "flr_pipe.cuh"
+
+namespace flr {
+
+constexpr int kSeg = 128;       // pixels per segment row (32 lanes x 4)
+constexpr int kApplyNCol = 18;  // model columns an APPLY item can touch (128/8 + 2)
+
+template <int Q>
+struct StreamDims {
+    static constexpr int NPF = Q + 3;                 // planes of a FIT row
+    static constexpr int MS = Dims<Q>::MSTRIDE;       // floats per padded model
+    static constexpr int MODF = 2 * kApplyNCol * MS;  // floats of an APPLY item's models
+    static constexpr int STG_FIT = NPF * kSeg;  // (Q+3) * 512 B: a multiple of 128 B
+    static constexpr int STG_APPLY = ((Q * kSeg > MODF ? Q * kSeg : MODF) + 31) / 32 * 32;
+};
+
+struct Ring {
+    float* stage;      // [S][STG]
+    uint64_t* full;    // [S]
+    int S, STG;
+    unsigned cons = 0;  // stages consumed (uniform across the warp)
+    unsigned prod = 0;  // stages produced (lane 0 only)
+    __device__ float* slot(unsigned i) const { return stage + (size_t)(i % S) * STG; }
+    __device__ uint64_t* bar(unsigned i) const { return &full[i % S]; }
+};
+
+// lane 0: issue stages until S are in flight or the sequence ends
+template <class Seq>
+__device__ __forceinline__ void ring_fill(Ring& r, Seq& q)
+{
+    while (r.prod < r.cons + r.S && q.next(r.slot(r.prod), r.bar(r.prod))) ++r.prod;
+}
+
+__device__ __forceinline__ const float* ring_wait(Ring& r)
+{
+    mbar_wait(r.bar(r.cons), (r.cons / r.S) & 1);
+    return r.slot(r.cons);
+}
+
+// all lanes done reading the current stage: release it and let lane 0 refill
+template <class Seq>
+__device__ __forceinline__ void ring_release(Ring& r, Seq& q, int lane)
+{
+    __syncwarp();
+    ++r.cons;
+    if (lane == 0) {
+#ifndef FLR_DBG_NOFENCE
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+        ring_fill(r, q);
+    }
+}
+
+// ============================================================================
+// FIT item: frame f, block row by, segment sg (fit pixels [128 sg, 128 sg + 128)).
+// ============================================================================
+struct FitArgs {
+    CUtensorMap tg;  // guides   [n*Q][H][W], box {128, 1, Q}
+    CUtensorMap ty;  // radiance [n*3][H][W], box {128, 1, 3}
+    double* mom;     // [n][KM][By][Bxp]
+    int W, H, Bx, Bxp, By, nseg;
+};
+
+template <int Q, int D>
+__device__ __forceinline__ void fit_issue_row(const FitArgs& a, int f, int by, int sg, int rr, float* dst,
+                                              uint64_t* bar, uint64_t pol_g, uint64_t pol_y)
+{
+    mbar_arrive_expect_tx(bar, (Q + 3) * kSeg * 4);
+    const int x = sg * kSeg, y = by * D + rr;
+    tma_load_3d(dst, &a.tg, x, y, f * Q, bar, pol_g);
+    tma_load_3d(dst + Q * kSeg, &a.ty, x, y, f * 3, bar, pol_y);
+}
+
+// packed-pair layout of the FIT accumulators: d is paired over planes (2p, 2p+1)
+template <int Q>
+struct FitPack {
+    static constexpr int QP = (Q + 1) / 2;
+    __host__ __device__ static constexpr int s2_base(int i)
+    {
+        int b = 0;
+        for (int t = 0; t < i; ++t) b += QP - t / 2;
+        return b;
+    }
+    static constexpr int NS2 = s2_base(Q);
+    __host__ __device__ static constexpr int s2(int i, int p) { return s2_base(i) + p - i / 2; }  // p >= i/2
+};
+
+template <int Q, int D, class Seq>
+__device__ __forceinline__ void fit_consume(Ring& r, Seq& q, const FitArgs& a, int f, int by, int sg, int lane)
+{
+    using Dm = Dims<Q>;
+    using FP = FitPack<Q>;
+    constexpr int DQ = D / 4, QP = FP::QP;
+    const int x0 = sg * kSeg + lane * 4;
+    const int bx = x0 / D;
+    const int lb0 = (lane / DQ) * D;  // first pixel of the lane's block within the segment
+    const int rows = min(D, a.H - by * D);
+
+    float c[2 * QP];
+    f2 U2[QP], S2[FP::NS2], XY2[3][QP], Y2[3];
+#pragma unroll
+    for (int p = 0; p < QP; ++p) U2[p] = 0ull;
+#pragma unroll
+    for (int s = 0; s < FP::NS2; ++s) S2[s] = 0ull;
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+        Y2[cc] = 0ull;
+#pragma unroll
+        for (int p = 0; p < QP; ++p) XY2[cc][p] = 0ull;
+    }
+
+    for (int rr = 0; rr < rows; ++rr) {
+        const float* st = ring_wait(r);
+        if (rr == 0) {
+#pragma unroll
+            for (int j = 0; j < 2 * QP; ++j) c[j] = j < Q ? st[j * kSeg + lb0] : 0.f;  // block's top-left pixel
+        }
+        // two pixel pairs per lane: 8-byte shared loads keep the live set small
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float g[Q][2], yv[3][2];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) {
+                const float2 v = reinterpret_cast<const float2*>(st + j * kSeg)[2 * lane + h];
+                g[j][0] = v.x; g[j][1] = v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const float2 v = reinterpret_cast<const float2*>(st + (Q + j) * kSeg)[2 * lane + h];
+                yv[j][0] = v.x; yv[j][1] = v.y;
+            }
+            if (h == 1) ring_release(r, q, lane);
+            // pixels beyond the image arrive as zeros: make them contribute nothing
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                if (x0 + 2 * h + k >= a.W) {
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) g[j][k] = c[j];
+                }
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) Y2[cc] = add2(Y2[cc], pk2(yv[cc][0], yv[cc][1]));
+#ifndef FLR_DBG_NOCOMPUTE
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                float d[2 * QP];
+#pragma unroll
+                for (int j = 0; j < 2 * QP; ++j) d[j] = j < Q ? g[j][k] - c[j] : 0.f;
+                f2 d2[QP];
+#pragma unroll
+                for (int p = 0; p < QP; ++p) {
+                    d2[p] = pk2(d[2 * p], d[2 * p + 1]);
+                    U2[p] = add2(U2[p], d2[p]);
+                }
+#pragma unroll
+                for (int i = 0; i < Q; ++i)
+#pragma unroll
+                    for (int p = i / 2; p < QP; ++p) S2[FP::s2(i, p)] = fma2(bc2(d[i]), d2[p], S2[FP::s2(i, p)]);
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+                    for (int p = 0; p < QP; ++p) XY2[cc][p] = fma2(bc2(yv[cc][k]), d2[p], XY2[cc][p]);
+            }
+#else
+            S2[0] = add2(S2[0], pk2(g[0][0], g[Q - 1][1]));
+#endif
+        }
+    }
+#pragma unroll
+    for (int m = 1; m < DQ; m <<= 1) {
+#pragma unroll
+        for (int p = 0; p < QP; ++p) U2[p] = add2(U2[p], __shfl_xor_sync(0xffffffffu, U2[p], m));
+#pragma unroll
+        for (int s = 0; s < FP::NS2; ++s) S2[s] = add2(S2[s], __shfl_xor_sync(0xffffffffu, S2[s], m));
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+            Y2[cc] = add2(Y2[cc], __shfl_xor_sync(0xffffffffu, Y2[cc], m));
+#pragma unroll
+            for (int p = 0; p < QP; ++p) XY2[cc][p] = add2(XY2[cc][p], __shfl_xor_sync(0xffffffffu, XY2[cc][p], m));
+        }
+    }
+    if (bx >= a.Bx) return;
+    // un-shift in fp64 (x = d + c) and store; lane gi of the block's DQ lanes writes k = gi mod DQ
+    double u[Q], yc[3];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) u[j] = (double)((j & 1) ? hi2(U2[j / 2]) : lo2(U2[j / 2]));
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) yc[cc] = (double)lo2(Y2[cc]) + (double)hi2(Y2[cc]);
+    const int gi = lane % DQ;
+    const double n = (double)(min(D, a.W - bx * D) * rows);
+    const size_t cs = (size_t)a.By * a.Bxp;
+    double* out = a.mom + (size_t)f * Dm::KM * cs + (size_t)by * a.Bxp + bx;
+    auto put = [&](int k, double v) {
+#ifndef FLR_DBG_NOSTORE
+        if (k % DQ == gi) out[(size_t)k * cs] = v;
+#else
+        if (v == 12345.678) out[(size_t)k * cs] = v;
+#endif
+    };
+    put(Dm::C_N, n);
+#pragma unroll
+    for (int j = 0; j < Q; ++j) put(Dm::C_U + j, fma(n, (double)c[j], u[j]));
+    // S_ij = S'_ij + c_i u'_j + c_j u'_i + n c_i c_j (compile-time (i, j): the accumulators stay in registers)
+    static_for<Q>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        static_for<Q - i>([&](auto JJ) {
+            constexpr int j = i + decltype(JJ)::value;
+            const f2 sp = S2[FP::s2(i, j / 2)];
+            double v = (double)((j & 1) ? hi2(sp) : lo2(sp));
+            v = fma((double)c[i], u[j], v);
+            v = fma((double)c[j], u[i], v);
+            v = fma(n * (double)c[i], (double)c[j], v);
+            put(Dm::s_idx(i, j), v);
+        });
+    });
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) put(Dm::C_Y + cc, yc[cc]);
+#pragma unroll
+    for (int j = 0; j < Q; ++j)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+            const f2 xp = XY2[cc][j / 2];
+            put(Dm::C_XY + j * 3 + cc, fma((double)c[j], yc[cc], (double)((j & 1) ? hi2(xp) : lo2(xp))));
+        }
+}
+
+// ============================================================================
+// APPLY item: frame f, row tile ty (output rows [8 ty - off, 8 ty - off + 8)), segment
+// sg (output pixels [128 sg - off, 128 sg - off + 128)), off = (D/2) % 8.  Every row of
+// the tile and every 4-pixel quad of the segment has one pair of bracketing block
+// centres (b + 1/2) D - 1/2 (R4), because D % 8 == 0.
+// ============================================================================
+struct ApplyArgs {
+    CUtensorMap tg;       // output-resolution guides [n*Q][H][W], box {128, 1, Q}
+    const float* models;  // [n][By][Bx][MS]
+    float* out;           // [n][3][H][W]
+    int W, H, D, Bx, By, nseg, ntile;
+};
+
+struct ApplyGeom {
+    int y0, y1;   // valid rows [y0, y1)
+    int xs;       // first pixel of the segment (may be < 0)
+    int j0, j1;   // bracketing block rows (clamped)
+    int ic0, nc;  // first staged model column, number staged
+};
+
+__device__ __forceinline__ ApplyGeom apply_geom(const ApplyArgs& a, int ty, int sg)
+{
+    ApplyGeom g;
+    const int off = (a.D / 2) % 8;
+    const float invD = 1.0f / (float)a.D;
+    const int ya = ty * 8 - off;
+    g.y0 = max(ya, 0);
+    g.y1 = min(ya + 8, a.H);
+    g.xs = sg * kSeg - off;
+    const int x0 = max(g.xs, 0);
+    const int jb = (int)floorf(((float)g.y0 + 0.5f) * invD - 0.5f);
+    g.j0 = min(max(jb, 0), a.By - 1);
+    g.j1 = min(max(jb + 1, 0), a.By - 1);
+    g.ic0 = min(max((int)floorf(((float)x0 + 0.5f) * invD - 0.5f), 0), a.Bx - 1);
+    g.nc = min(kApplyNCol, a.Bx - g.ic0);
+    return g;
+}
+
+// model stage: the two rows of block models [j][ic0 .. ic0+nc) (lane 0)
+template <int Q>
+__device__ __forceinline__ void apply_issue_models(const ApplyArgs& a, const ApplyGeom& g, int f, float* dst,
+                                                   uint64_t* bar, uint64_t pol_m)
+{
+    using SD = StreamDims<Q>;
+    const unsigned mb = (unsigned)(g.nc * SD::MS * 4);
+    mbar_arrive_expect_tx(bar, 2 * mb);
+    const float* M = a.models + (size_t)f * a.By * a.Bx * SD::MS;
+    bulk_g2s(dst, M + ((size_t)g.j0 * a.Bx + g.ic0) * SD::MS, mb, bar, pol_m);
+    bulk_g2s(dst + kApplyNCol * SD::MS, M + ((size_t)g.j1 * a.Bx + g.ic0) * SD::MS, mb, bar, pol_m);
+}
+
+// guide row y of an APPLY item (lane 0)
+template <int Q>
+__device__ __forceinline__ void apply_issue_row(const ApplyArgs& a, const ApplyGeom& g, int f, int y, float* dst,
+                                                uint64_t* bar, uint64_t pol_g)
+{
+    mbar_arrive_expect_tx(bar, Q * kSeg * 4);
+    tma_load_3d(dst, &a.tg, g.xs, y, f * Q, bar, pol_g);
+}
+
+// stream warp.  `mod` = per-warp [2][kApplyNCol][MS] raw models, `lerp` = [kApplyNCol][MS].
+template <int Q, class Seq>
+__device__ __forceinline__ void apply_consume(Ring& r, Seq& sq, const ApplyArgs& a, int f, int ty, int sg, int lane,
+                                              float* mod, float* lerp)
+{
+    using SD = StreamDims<Q>;
+    constexpr int MS = SD::MS, P = Q + 1;
+    const ApplyGeom g = apply_geom(a, ty, sg);
+    const float invD = 1.0f / (float)a.D;
+    {  // models: copy out of the ring so the stage can be refilled at once
+        const float* st = ring_wait(r);
+        const float4* s4 = reinterpret_cast<const float4*>(st);
+        float4* d4 = reinterpret_cast<float4*>(mod);
+        for (int i = lane; i < 2 * kApplyNCol * MS / 4; i += 32) d4[i] = s4[i];
+        ring_release(r, sq, lane);
+    }
+    const int xq = g.xs + lane * 4;  // the lane's quad
+    const bool active = xq >= 0 && xq < a.W;
+    const float fxq = ((float)max(xq, 0) + 0.5f) * invD - 0.5f;
+    const int ib = (int)floorf(fxq);
+    const int c0 = min(max(ib, 0), a.Bx - 1) - g.ic0;
+    const int c1 = min(max(ib + 1, 0), a.Bx - 1) - g.ic0;
+    f2 t2[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        t2[h] = pk2(((float)(xq + 2 * h) + 0.5f) * invD - 0.5f - (float)ib,
+                    ((float)(xq + 2 * h + 1) + 0.5f) * invD - 0.5f - (float)ib);
+    const size_t plane = (size_t)a.W * a.H;
+    float* O = a.out + (size_t)f * 3 * plane;
+    for (int y = g.y0; y < g.y1; ++y) {
+        const float fy = ((float)y + 0.5f) * invD - 0.5f;
+        const float tyy = fy - floorf(fy);
+        // y-blend the staged model columns once per row for the whole warp
+        for (int i = lane; i < g.nc * (MS / 4); i += 32) {
+            const float4 p = reinterpret_cast<const float4*>(mod)[i];
+            const float4 q = reinterpret_cast<const float4*>(mod + kApplyNCol * MS)[i];
+            reinterpret_cast<float4*>(lerp)[i] =
+                make_float4(fmaf(tyy, q.x - p.x, p.x), fmaf(tyy, q.y - p.y, p.y), fmaf(tyy, q.z - p.z, p.z),
+                            fmaf(tyy, q.w - p.w, p.w));
+        }
+        __syncwarp();
+        const float* st = ring_wait(r);
+        float gq[Q][4];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+            const float4 v = reinterpret_cast<const float4*>(st + j * kSeg)[lane];
+            gq[j][0] = v.x; gq[j][1] = v.y; gq[j][2] = v.z; gq[j][3] = v.w;
+        }
+        ring_release(r, sq, lane);
+        float m0[4 * (MS / 4)], m1[4 * (MS / 4)];
+#pragma unroll
+        for (int v = 0; v < MS / 4; ++v) {
+            const float4 p = reinterpret_cast<const float4*>(lerp + c0 * MS)[v];
+            const float4 q = reinterpret_cast<const float4*>(lerp + c1 * MS)[v];
+            m0[4 * v] = p.x; m0[4 * v + 1] = p.y; m0[4 * v + 2] = p.z; m0[4 * v + 3] = p.w;
+            m1[4 * v] = q.x; m1[4 * v + 1] = q.y; m1[4 * v + 2] = q.z; m1[4 * v + 3] = q.w;
+        }
+        __syncwarp();  // `lerp` is rewritten for the next row
+        float o[3][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // pixel pairs (2h, 2h+1)
+            f2 gp[Q];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) gp[j] = pk2(gq[j][2 * h], gq[j][2 * h + 1]);
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                f2 p0 = bc2(m0[cc]), p1 = bc2(m1[cc]);
+#pragma unroll
+                for (int j = 0; j < Q; ++j) {
+                    p0 = fma2(gp[j], bc2(m0[(1 + j) * 3 + cc]), p0);
+                    p1 = fma2(gp[j], bc2(m1[(1 + j) * 3 + cc]), p1);
+                }
+                upk2(fma2(t2[h], sub2(p1, p0), p0), o[cc][2 * h], o[cc][2 * h + 1]);
+            }
+        }
+        if (active) {
+            float* Orow = O + (size_t)y * a.W + xq;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+                asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(Orow + cc * plane), "f"(o[cc][0]),
+                             "f"(o[cc][1]), "f"(o[cc][2]), "f"(o[cc][3])
+                             : "memory");
+        }
+        (void)P;
+    }
+}
+
+}  // namespace flr

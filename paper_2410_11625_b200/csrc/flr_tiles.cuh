@@ -6,7 +6,10 @@
 // Full-resolution planes are streamed once per pass with 16-byte loads; all
 // intermediates live at block resolution.
 #pragma once
+#include <cuda.h>
+
 #include "flr_common.cuh"
+#include "flr_pipe.cuh"
 #include "flr_solve.cuh"
 
 namespace flr {
@@ -78,7 +81,7 @@ constexpr size_t fit_smem_bytes()
 }
 
 template <int Q, int D, bool VEC>
-__global__ void __launch_bounds__(FitGeom<D>::THREADS) k_fit_moments(int W, int H, int Bx, int By,
+__global__ void __launch_bounds__(FitGeom<D>::THREADS) k_fit_moments(int W, int H, int Bx, int Bxp, int By,
                                                                      const float* __restrict__ guides,
                                                                      const float* __restrict__ radiance,
                                                                      double* __restrict__ mom)
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(FitGeom<D>::THREADS) k_fit_moments(int W, int 
     constexpr int KA = Dm::KM - 1;  // accumulated components (all but n), index a = k - 1
     constexpr int KP = KA | 1;
     constexpr int NS = Dm::NS;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     double* tot = reinterpret_cast<double*>(smem_raw);                      // [NB][KA]
     float* part = reinterpret_cast<float*>(tot + G::NB * KA);              // [NW][NB][KP]
     float* csh = part + G::NW * G::NB * KP;                                // [NB][Q]
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(FitGeom<D>::THREADS) k_fit_moments(int W, int 
     __syncthreads();
     // un-shift (fp64) and store the moment field, coalesced along bx
     const int rows = min(D, H - by * D);
-    const size_t cs = (size_t)By * Bx;
+    const size_t cs = (size_t)By * Bxp;
     for (int i = threadIdx.x; i < G::NB * Dm::KM; i += G::THREADS) {
         const int b = i % G::NB, k = i / G::NB;
         const int bxg = seg * G::NB + b;
@@ -239,27 +242,31 @@ __global__ void __launch_bounds__(FitGeom<D>::THREADS) k_fit_moments(int W, int 
             const int j = (k - Dm::C_XY) / 3, cc = (k - Dm::C_XY) % 3;
             v = fma((double)cb[j], T[Dm::C_Y + cc - 1], T[k - 1]);
         }
-        mom[((size_t)f * Dm::KM + k) * cs + (size_t)by * Bx + bxg] = v;
+        mom[((size_t)f * Dm::KM + k) * cs + (size_t)by * Bxp + bxg] = v;
     }
 }
 
 // ===========================================================================
 // K2: blur + solve.  One CTA = TX x TY output blocks (one thread each).  For each
-// group of G moment components: cp.async the (TY+2R) x (TX+2R) halo of the fp64
-// moment field into shared memory (zero outside the grid = zero padding, R3;
-// double-buffered), vertical pass -> TY x (TX+2R), horizontal pass -> registers.
-// Then the appendix solve per thread (flr_solve.cuh).  R <= kTileMaxR.
+// group of G moment components, ONE 3-D TMA load brings the (TY+2R) x (TX+2R) halo
+// of the pitched fp64 moment field into shared memory (out-of-grid blocks read as
+// zero = the zero padding of R3; double-buffered on two mbarriers); a vertical
+// pass -> TY x (TX+2R) and a horizontal pass -> registers (P:299-309, P:316,
+// P:334); then the appendix solve per thread (flr_solve.cuh).  R <= kTileMaxR.
 // ===========================================================================
 constexpr int kTileTX = 32, kTileTY = 4, kTileG = 12, kTileMaxR = 8;
 
+// TMA box starts must be 16-byte aligned: the x halo is rounded up to an even count
+__host__ __device__ constexpr int halo_x(int R) { return kTileTX + 2 * ((R + 1) & ~1); }
+
 inline size_t blur_solve_smem_bytes(int R)
 {
-    const int HX = kTileTX + 2 * R, HY = kTileTY + 2 * R;
-    return (size_t)(2 * kTileG * HY * HX + kTileG * kTileTY * HX) * sizeof(double);
+    const int HX = halo_x(R), HY = kTileTY + 2 * R;
+    return (size_t)(2 * kTileG * HY * HX + kTileG * kTileTY * HX) * sizeof(double) + 2 * sizeof(uint64_t);
 }
 
 template <int Q, int R>
-__global__ void __launch_bounds__(kTileTX* kTileTY) k_blur_solve(int Bx, int By, const double* __restrict__ mom,
+__global__ void __launch_bounds__(kTileTX* kTileTY) k_blur_solve(const __grid_constant__ CUtensorMap tm, int Bx, int By,
                                                                 float* __restrict__ models, int mstride,
                                                                 double eps_add, double eps_mul,
                                                                 const __grid_constant__ Taps t)
@@ -267,47 +274,41 @@ __global__ void __launch_bounds__(kTileTX* kTileTY) k_blur_solve(int Bx, int By,
     using Dm = Dims<Q>;
     constexpr int KM = Dm::KM, GG = kTileG, NG = (KM + GG - 1) / GG;
     constexpr int TX = kTileTX, TY = kTileTY, NT = TX * TY;
-    constexpr int HX = TX + 2 * R, HY = TY + 2 * R, NTAP = 2 * R + 1;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* sm = reinterpret_cast<double*>(smem_raw);
-    double* halo0 = sm;
-    double* halo1 = sm + GG * HY * HX;
-    double* vb = sm + 2 * GG * HY * HX;
+    constexpr int RE = (R + 1) & ~1;  // x halo (even: 16-byte aligned TMA box start)
+    constexpr int HX = halo_x(R), HY = TY + 2 * R, NTAP = 2 * R + 1;
+    constexpr unsigned BOX_BYTES = GG * HY * HX * sizeof(double);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double* halo[2] = {reinterpret_cast<double*>(smem_raw), reinterpret_cast<double*>(smem_raw) + GG * HY * HX};
+    double* vb = halo[1] + GG * HY * HX;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(vb + GG * TY * HX);
     const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
     const int bx0 = blockIdx.x * TX, by0 = blockIdx.y * TY, f = blockIdx.z;
-    const size_t cs = (size_t)By * Bx;
-    const double* momf = mom + (size_t)f * KM * cs;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
     double g[NTAP];
 #pragma unroll
     for (int d = 0; d < NTAP; ++d) g[d] = t.g[d];
-
-    auto issue = [&](int grp, double* buf) {
-        constexpr int n = GG * HY * HX;
-        for (int i = threadIdx.x; i < n; i += NT) {
-            const int gi = i / (HY * HX), r = (i / HX) % HY, cc = i % HX;
-            const int k = grp * GG + gi, yy = by0 - R + r, xx = bx0 - R + cc;
-            const bool ok = k < KM && yy >= 0 && yy < By && xx >= 0 && xx < Bx;
-            const double* src = ok ? momf + (size_t)k * cs + (size_t)yy * Bx + xx : momf;
-            cp_async8(buf + i, src, ok ? 8 : 0);
-        }
-        cp_async_commit();
+    const uint64_t pol = policy_evict_normal();
+    auto issue = [&](int grp) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the buffer
+        mbar_arrive_expect_tx(&bar[grp & 1], BOX_BYTES);
+        tma_load_3d(halo[grp & 1], &tm, bx0 - RE, by0 - R, f * KM + grp * GG, &bar[grp & 1], pol);
     };
+    if (threadIdx.x == 0) issue(0);
 
     double blur[KM];
-    issue(0, halo0);
 #pragma unroll
     for (int grp = 0; grp < NG; ++grp) {
-        double* h = (grp & 1) ? halo1 : halo0;
-        if (grp + 1 < NG) {
-            issue(grp + 1, (grp & 1) ? halo0 : halo1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
+        if (threadIdx.x == 0 && grp + 1 < NG) issue(grp + 1);  // buffer (grp+1)&1 was released by the last sync
+        mbar_wait(&bar[grp & 1], (grp >> 1) & 1);
+        const double* h = halo[grp & 1];
         // vertical pass: one thread per (component, halo column), TY outputs from HY loads
         for (int col = threadIdx.x; col < GG * HX; col += NT) {
-            const int gi = col / HX, cc = col % HX;
+            const int gi = col / HX, cc = col - gi * HX;
             const double* src = h + gi * HY * HX + cc;
             double v[HY];
 #pragma unroll
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(kTileTX* kTileTY) k_blur_solve(int Bx, int By,
         for (int gi = 0; gi < GG; ++gi) {
             const int k = grp * GG + gi;
             if (k < KM) {
-                const double* src = vb + (gi * TY + ty) * HX + tx;
+                const double* src = vb + (gi * TY + ty) * HX + tx + (RE - R);
                 double acc = 0.0;
 #pragma unroll
                 for (int d = 0; d < NTAP; ++d) acc = fma(g[d], src[d], acc);
@@ -337,8 +338,12 @@ __global__ void __launch_bounds__(kTileTX* kTileTY) k_blur_solve(int Bx, int By,
     }
     const int bx = bx0 + tx, by = by0 + ty;
     if (bx >= Bx || by >= By) return;
+#ifdef FLR_DBG_BLUR_NOSOLVE
+    models[((size_t)(f * By + by) * Bx + bx) * mstride] = (float)(blur[0] + blur[KM - 1]);
+#else
     solve_block<Q>([&](int k) { return blur[k]; }, eps_add, eps_mul,
                    models + ((size_t)(f * By + by) * Bx + bx) * mstride);
+#endif
 }
 
 // ===========================================================================
