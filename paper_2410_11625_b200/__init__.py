@@ -20,7 +20,7 @@ import os
 
 __all__ = ["FLRError", "Params", "lib", "lib_path", "workspace_size", "effective_radius", "fit",
            "apply", "denoise", "denoise_upsample", "Denoiser", "EventTrace", "last_launch_count", "last_launch_names",
-           "VARIANT_AUTO", "VARIANT_STAGED"]
+           "VARIANT_AUTO", "VARIANT_STAGED", "VARIANT_FUSED"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_PKG, "libflr.so")
@@ -28,6 +28,7 @@ _lib = None
 
 VARIANT_AUTO = 0
 VARIANT_STAGED = 1
+VARIANT_FUSED = 2
 
 
 class EventTrace(ctypes.Structure):

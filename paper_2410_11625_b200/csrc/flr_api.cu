@@ -28,7 +28,8 @@ flr_status check_params(const flr_params* p)
     if (!(p->eps_add >= 0.0) || !std::isfinite(p->eps_add)) return FLR_ERR_INVALID_VALUE;
     if (!(p->eps_mul >= 0.0) || !(p->eps_mul < 1.0)) return FLR_ERR_INVALID_VALUE;
     if (p->radius < 0) return FLR_ERR_INVALID_VALUE;
-    if (p->variant != FLR_VARIANT_AUTO && p->variant != FLR_VARIANT_STAGED) return FLR_ERR_UNSUPPORTED;
+    if (p->variant != FLR_VARIANT_AUTO && p->variant != FLR_VARIANT_STAGED && p->variant != FLR_VARIANT_FUSED)
+        return FLR_ERR_UNSUPPORTED;
     return FLR_OK;
 }
 
@@ -41,7 +42,7 @@ int effective_radius(const flr_params* p)
 }
 
 struct Layout {
-    size_t raw, mom, hb, models, total;
+    size_t raw, mom, hb, models, flags, total;
 };
 
 // workspace: raw fp32 moments | fp64 un-shifted moments | fp64 x-blurred | padded models
@@ -59,6 +60,8 @@ Layout layout(int n, int Q, int Bx, int By)
     off += align256(nbp * km_of(Q) * sizeof(double));
     L.models = off;
     off += align256(nb * mstride_of(Q) * sizeof(float));
+    L.flags = off;  // fused schedule: fit_done [n][By] + solve_done [n][ceil(By/4)]
+    off += align256(sizeof(int) * (size_t)n * (By + (By + 3) / 4));
     L.total = off;
     return L;
 }
@@ -268,6 +271,20 @@ flr_status flr_denoise_upsample_traced(int32_t n, int32_t Q, int32_t W_lo, int32
     float* models = (float*)((char*)workspace + L.models);
     const int ms = mstride_of(Q);
     LaunchCtx ctx = make_ctx(stream, trace);
+    if (p->variant != FLR_VARIANT_STAGED) {
+        FusedLaunch F;
+        F.n = n, F.W = W_lo, F.H = H_lo, F.D = D, F.U = p->upsample, F.Bx = Bx, F.By = By;
+        F.G = guides_lo, F.Y = radiance_lo, F.Gout = guides_hi, F.out = out;
+        F.mom = (double*)((char*)workspace + L.mom);
+        F.models = models;
+        F.flags = (int*)((char*)workspace + L.flags);
+        F.eps_add = p->eps_add, F.eps_mul = p->eps_mul;
+        F.taps = make_taps(p->sigma / ((double)D * p->upsample), effective_radius(p));
+        bool done = false;
+        FLR_DISPATCH_Q(Q, (done = launch_fused<QQ>(F, ctx)));
+        if (done) return finish(ctx, trace);
+        if (p->variant == FLR_VARIANT_FUSED) return FLR_ERR_UNSUPPORTED;
+    }
     if ((st = do_fit(n, Q, W_lo, H_lo, guides_lo, radiance_lo, p, models, ms, workspace, ctx)))
         return st;
     const int Dout = D * p->upsample;

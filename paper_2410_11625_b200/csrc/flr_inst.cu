@@ -6,6 +6,12 @@
 #include "flr_staged.cuh"
 #include "flr_tiles.cuh"
 #include "flr_persist.cuh"
+#if FLR_Q == 4 || FLR_Q == 8
+#include "flr_fused.cuh"
+#endif
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 namespace flr {
 
@@ -22,11 +28,35 @@ void launch_apply(int, int, int, int, int, int, const float*, int, const float*,
 {
     ctx.unsupported = true;
 }
+template <int Q>
+bool launch_fused(const FusedLaunch&, LaunchCtx&)
+{
+    return false;
+}
 #else
 template <class K>
 static void set_smem(K kernel, size_t bytes)
 {
     if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// launch with programmatic stream serialization (PDL): the grid may start while the
+// previous grid in the stream drains; kernels call pdl_wait() before touching its output
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args)
+{
+    static const bool off = std::getenv("FLR_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 static int num_sms()
@@ -50,7 +80,7 @@ static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
         const int items = n * By * a.nseg;
         const int grid = min(num_sms(), cdiv(items, C::NSW));
         set_smem(k_fit_stream<Q, D>, C::SMEM);
-        k_fit_stream<Q, D><<<grid, C::THREADS, C::SMEM, s>>>(a, n);
+        launch_pdl(k_fit_stream<Q, D>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
         return;
     }
     const size_t sm = fit_smem_bytes<Q, D>();
@@ -84,12 +114,28 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
         const int nb = Bx * By;
         k_unshift<Q><<<dim3(cdiv(nb, 128), n), 128, 0, s>>>(Bx, mom_pitch(Bx), By, raw, mom);
     }
-    // K2: blur + solve -> models
+    // K2: blur (component-parallel, fp64) -> hb, then solve (thread per block) -> models
     CUtensorMap tm;
     const int Bxp = mom_pitch(Bx), R = taps.R;
-    if (R >= 1 && R <= kTileMaxR &&
+    constexpr int NGRP = (Dims<Q>::KM + kBlurG - 1) / kBlurG;
+    if (R >= 1 && R <= kTileMaxR && !std::getenv("FLR_TILE_SOLVE") &&
+        make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, blur_halo_x(R),
+                     kBlurTY + 2 * R, kBlurG)) {
+        ctx.before("k_blur");
+        const dim3 grid(cdiv(Bx, kBlurTX), cdiv(By, kBlurTY), n * NGRP);
+#define FLR_KB(RR)                                                                                  \
+    case RR:                                                                                        \
+        set_smem(k_blur<Q, RR>, BlurGeom<RR>::SMEM);                                                \
+        launch_pdl(k_blur<Q, RR>, grid, dim3(256), BlurGeom<RR>::SMEM, s, tm, Bx, Bxp, By, hb, taps); \
+        break;
+        switch (R) { FLR_KB(1) FLR_KB(2) FLR_KB(3) FLR_KB(4) FLR_KB(5) FLR_KB(6) FLR_KB(7) FLR_KB(8) }
+#undef FLR_KB
+        ctx.before("k_solve");
+        launch_pdl(k_solve<Q>, dim3(cdiv(Bx, 128), By, n), dim3(128), 0, s, Bx, Bxp, By, (const double*)hb, models,
+                   mstride, ea, em);
+    } else if (R >= 1 && R <= kTileMaxR &&
         make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, halo_x(R),
-                     kTileTY + 2 * R, kTileG)) {
+                     kTileTY + 2 * R, tile_g(R))) {
         ctx.before("k_blur_solve");
         const size_t sm = blur_solve_smem_bytes(taps.R);
         const dim3 grid(cdiv(Bx, kTileTX), cdiv(By, kTileTY), n), block(kTileTX * kTileTY);
@@ -122,13 +168,13 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
         ApplyArgs a;
         if (vec_ok(G, W) && vec_ok(out, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q)) {  // TMA path
             a.models = models, a.out = out;
-            a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W + off, kSeg), a.ntile = cdiv(H + off, 8);
+            a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W, kSeg), a.nband = apply_nband(H, D, By);
             using C = ApplyCfg<Q>;
-            const int items = n * a.nseg * a.ntile;
+            const int items = n * a.nseg * a.nband;
             const int grid = min(num_sms(), cdiv(items, C::NSW));
             ctx.before("k_apply_stream");
             set_smem(k_apply_stream<Q>, C::SMEM);
-            k_apply_stream<Q><<<grid, C::THREADS, C::SMEM, s>>>(a, n);
+            launch_pdl(k_apply_stream<Q>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
             return;
         }
         dim3 grid(cdiv(cdiv(W + off, 8), kApplyUnits), cdiv(H + off, kApplyRows), n),
@@ -145,6 +191,67 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
     }
 }
 
+template <int Q>
+bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx)
+{
+#if FLR_Q == 4 || FLR_Q == 8
+    const int Dout = L.D * L.U, R = L.taps.R;
+    const int Wo = L.W * L.U, Ho = L.H * L.U;
+    if (!(L.D == 4 || L.D == 8) || Dout % 8 || !(R == 3 || R == 5)) return false;
+    if (!vec_ok(L.G, L.W) || !vec_ok(L.Y, L.W) || !vec_ok(L.Gout, Wo) || !vec_ok(L.out, Wo)) return false;
+    FusedArgs a;
+    std::memset(&a, 0, sizeof(a));
+    const int Bxp = mom_pitch(L.Bx);
+    if (!make_tmap_planes(&a.fit.tg, L.G, L.W, L.H, L.n * Q, kSeg, Q) ||
+        !make_tmap_planes(&a.fit.ty, L.Y, L.W, L.H, L.n * 3, kSeg, 3) ||
+        !make_tmap_planes(&a.app.tg, L.Gout, Wo, Ho, L.n * Q, kSeg, Q) ||
+        !make_tmap_3d(&a.tmom, L.mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, L.Bx, L.By, Bxp, L.n * Dims<Q>::KM,
+                      halo_x(R), kTileTY + 2 * R, tile_g(R)))
+        return false;
+    a.fit.mom = L.mom;
+    a.fit.W = L.W, a.fit.H = L.H, a.fit.Bx = L.Bx, a.fit.Bxp = Bxp, a.fit.By = L.By, a.fit.nseg = cdiv(L.W, kSeg);
+    a.app.models = L.models, a.app.out = L.out;
+    a.app.W = Wo, a.app.H = Ho, a.app.D = Dout, a.app.Bx = L.Bx, a.app.By = L.By;
+    a.app.nseg = cdiv(Wo, kSeg), a.app.nband = apply_nband(Ho, Dout, L.By);
+    a.taps = L.taps;
+    a.nrt = cdiv(L.By, kTileTY), a.ncx = cdiv(L.Bx, kTileTX);
+    a.fit_done = L.flags;
+    a.solve_done = L.flags + L.n * L.By;
+    a.n = L.n;
+    int lag = 32 + R;  // block rows between a FIT and the APPLY that reuses its guides (tunable)
+    if (const char* e = std::getenv("FLR_FUSED_LAG")) lag = std::max(R + kTileTY + 1, std::atoi(e));
+    a.lag = lag;
+    a.eps_add = L.eps_add, a.eps_mul = L.eps_mul;
+    cudaMemsetAsync(L.flags, 0, sizeof(int) * (size_t)L.n * (L.By + a.nrt), ctx.s);
+
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3(num_sms());
+    cfg.blockDim = dim3(kFusedThreads);
+    cfg.stream = ctx.s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#define FLR_FUSED(DD, RR)                                                                        \
+    if (L.D == DD && R == RR) {                                                                  \
+        using C = FusedCfg<Q, RR>;                                                               \
+        cfg.dynamicSmemBytes = C::SMEM;                                                          \
+        set_smem(k_flr_fused<Q, DD, RR>, C::SMEM);                                               \
+        ctx.before("k_flr_fused");                                                               \
+        cudaLaunchKernelEx(&cfg, k_flr_fused<Q, DD, RR>, a);                                     \
+        return true;                                                                             \
+    }
+    FLR_FUSED(4, 3) FLR_FUSED(4, 5) FLR_FUSED(8, 3) FLR_FUSED(8, 5)
+#undef FLR_FUSED
+    return false;
+#else
+    (void)L;
+    (void)ctx;
+    return false;
+#endif
+}
+
 #endif  // FLR_STUB
 
 template void launch_fit<FLR_Q>(int, int, int, int, int, int, const float*, const float*, float*,
@@ -152,5 +259,6 @@ template void launch_fit<FLR_Q>(int, int, int, int, int, int, const float*, cons
                                 LaunchCtx&);
 template void launch_apply<FLR_Q>(int, int, int, int, int, int, const float*, int, const float*,
                                   float*, LaunchCtx&);
+template bool launch_fused<FLR_Q>(const FusedLaunch&, LaunchCtx&);
 
 }  // namespace flr

@@ -86,12 +86,29 @@ template <int Q>
 void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* models, int mstride,
                   const float* G, float* out, LaunchCtx& ctx);
 
+// the fused single-kernel schedule (flr_fused.cuh); returns false when this (Q, D_fit,
+// D_out, R, alignment) combination is not compiled in, so the caller falls back to the
+// staged kernels.  `flags` = 4 * n * (By + ceil(By/4)) bytes of workspace.
+struct FusedLaunch {
+    int n, W, H, D, U, Bx, By;              // fit resolution, block size, upsample
+    const float *G, *Y, *Gout;              // fit guides, fit radiance, output-resolution guides
+    float* out;
+    double* mom;
+    float* models;                          // padded [n][By][Bx][MSTRIDE]
+    int* flags;
+    double eps_add, eps_mul;
+    Taps taps;
+};
+template <int Q>
+bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx);
+
 #define FLR_DECLARE_Q(Q)                                                                          \
     extern template void launch_fit<Q>(int, int, int, int, int, int, const float*, const float*,  \
                                        float*, double*, double*, float*, int, double, double,     \
                                        const Taps&, LaunchCtx&);                          \
     extern template void launch_apply<Q>(int, int, int, int, int, int, const float*, int,         \
-                                         const float*, float*, LaunchCtx&);
+                                         const float*, float*, LaunchCtx&);                     \
+    extern template bool launch_fused<Q>(const FusedLaunch&, LaunchCtx&);
 FLR_DECLARE_Q(1) FLR_DECLARE_Q(2) FLR_DECLARE_Q(3) FLR_DECLARE_Q(4) FLR_DECLARE_Q(5)
 FLR_DECLARE_Q(6) FLR_DECLARE_Q(7) FLR_DECLARE_Q(8) FLR_DECLARE_Q(9) FLR_DECLARE_Q(10)
 FLR_DECLARE_Q(11) FLR_DECLARE_Q(12) FLR_DECLARE_Q(13) FLR_DECLARE_Q(14) FLR_DECLARE_Q(15)

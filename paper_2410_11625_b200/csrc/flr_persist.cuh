@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(FitCfg<Q>::THREADS, 1) k_fit_stream(const __gr
     const int GW = gridDim.x * C::NSW, first = blockIdx.x * C::NSW + w;
     Ring r = sm.ring(w);
     FitSeq<Q, D> seq{&a, first, 0, nitems, per_frame, GW, policy_evict_normal(), policy_evict_first()};
+    pdl_trigger();
+    pdl_wait();  // caller data may come from the previous grid: wait before the first read
     if (lane == 0) ring_fill(r, seq);
     for (int it = first; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it % per_frame;
@@ -127,10 +129,12 @@ __global__ void __launch_bounds__(ApplyCfg<Q>::THREADS, 1) k_apply_stream(const 
     sm.init_barriers();
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int per_frame = a.ntile * a.nseg, nitems = n * per_frame;
+    const int per_frame = a.nband * a.nseg, nitems = n * per_frame;
     const int GW = gridDim.x * C::NSW, first = blockIdx.x * C::NSW + w;
     Ring r = sm.ring(w);
     ApplySeq<Q> seq{&a, first, -1, nitems, per_frame, GW, policy_evict_first(), policy_evict_normal()};
+    pdl_trigger();
+    pdl_wait();  // models come from the previous grid
     if (lane == 0) ring_fill(r, seq);
     for (int it = first; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it % per_frame;

@@ -92,6 +92,12 @@ __device__ __forceinline__ void red_release_add(int* p, int v)
 
 namespace flr {
 
+// ---- programmatic dependent launch (no-ops when launched without the PDL attribute) ----
+// wait: block until the preceding grid in the stream has completed and flushed its writes
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// trigger: let the next grid in the stream start launching its CTAs now
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- TMA tensor load (3-D tile; coordinates may be negative: out-of-range elements are zero) ----
 __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z, uint64_t* bar,
                                             uint64_t policy)

@@ -4,6 +4,7 @@
 //   n = M_00, mu_X = u_X / n, mu_Y = N_0 / n
 //   W^ = S/n + eps_mul diag(mu^2) + eps_add I - (1 - eps_mul) mu mu^T (R7, R8)
 //   sigma^ = sqrt(max(diag W^, 1e-300))                            (R11)
+//   (only 1/sigma^ and 1/R_kk are needed: one rsqrt each, <= 1 ulp from sqrt-then-divide)
 //   C^_ij = W^_ij / (sigma^_i sigma^_j)
 //   B^_ic = (XY_ic / n - mu_i mu_Y,c) / sigma^_i                   (R9)
 //   A^ = (C^ + eps_add I)^-1 B^
@@ -41,7 +42,7 @@ __device__ __forceinline__ void solve_block(MomentFn&& m, double eps_add, double
         }
     double isig[Q];
 #pragma unroll
-    for (int i = 0; i < Q; ++i) isig[i] = 1.0 / sqrt(fmax(Wh[Dm::s_idx(i, i) - Dm::C_S], 1e-300));
+    for (int i = 0; i < Q; ++i) isig[i] = rsqrt(fmax(Wh[Dm::s_idx(i, i) - Dm::C_S], 1e-300));
     double muY[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) muY[c] = m(Dm::C_Y + c) * inv_n;
@@ -68,7 +69,7 @@ __device__ __forceinline__ void solve_block(MomentFn&& m, double eps_add, double
             const double r = Wh[Dm::s_idx(p, k) - Dm::C_S];
             dkk = fma(-r, r, dkk);
         });
-        rinv[k] = 1.0 / sqrt(dkk);
+        rinv[k] = rsqrt(dkk);
         static_for<Q - k - 1>([&](auto JJ) {
             constexpr int j = k + 1 + decltype(JJ)::value;
             double v = Wh[Dm::s_idx(k, j) - Dm::C_S];

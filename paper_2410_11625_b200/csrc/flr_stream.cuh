@@ -50,8 +50,19 @@ __device__ __forceinline__ void ring_fill(Ring& r, Seq& q)
     while (r.prod < r.cons + r.S && q.next(r.slot(r.prod), r.bar(r.prod))) ++r.prod;
 }
 
-__device__ __forceinline__ const float* ring_wait(Ring& r)
+// wait until the warp's next stage is filled.  If lane 0's cursor stopped at an item
+// whose dependency was not ready yet (Seq::next returned false), lane 0 keeps retrying
+// here, where the warp has nothing else to do.
+template <class Seq>
+__device__ __forceinline__ const float* ring_wait(Ring& r, Seq& q, int lane)
 {
+    if (lane == 0) {
+        while (r.prod <= r.cons) {
+            ring_fill(r, q);
+            if (r.prod <= r.cons) __nanosleep(256);
+        }
+    }
+    __syncwarp();
     mbar_wait(r.bar(r.cons), (r.cons / r.S) & 1);
     return r.slot(r.cons);
 }
@@ -129,7 +140,7 @@ __device__ __forceinline__ void fit_consume(Ring& r, Seq& q, const FitArgs& a, i
     }
 
     for (int rr = 0; rr < rows; ++rr) {
-        const float* st = ring_wait(r);
+        const float* st = ring_wait(r, q, lane);
         if (rr == 0) {
 #pragma unroll
             for (int j = 0; j < 2 * QP; ++j) c[j] = j < Q ? st[j * kSeg + lb0] : 0.f;  // block's top-left pixel
@@ -243,39 +254,41 @@ __device__ __forceinline__ void fit_consume(Ring& r, Seq& q, const FitArgs& a, i
 }
 
 // ============================================================================
-// APPLY item: frame f, row tile ty (output rows [8 ty - off, 8 ty - off + 8)), segment
-// sg (output pixels [128 sg - off, 128 sg - off + 128)), off = (D/2) % 8.  Every row of
-// the tile and every 4-pixel quad of the segment has one pair of bracketing block
-// centres (b + 1/2) D - 1/2 (R4), because D % 8 == 0.
+// APPLY item: frame f, band j (output rows [jD - D/2, jD + D/2) inside the image),
+// segment sg (output pixels [128 sg, 128 sg + 128)).  Every row of band j lies between
+// the block centres (b + 1/2) D - 1/2 of block rows j-1 and j (clamped, R4), and for
+// D % 8 == 0 every 4-pixel quad lies between one pair of block-centre columns.
 // ============================================================================
 struct ApplyArgs {
     CUtensorMap tg;       // output-resolution guides [n*Q][H][W], box {128, 1, Q}
     const float* models;  // [n][By][Bx][MS]
     float* out;           // [n][3][H][W]
-    int W, H, D, Bx, By, nseg, ntile;
+    int W, H, D, Bx, By, nseg, nband;
 };
 
+__host__ __device__ inline int apply_nband(int H, int D, int By)
+{
+    const int nb = (H + D / 2 + D - 1) / D;  // bands j with j*D - D/2 < H
+    return nb < By + 1 ? nb : By + 1;
+}
+
 struct ApplyGeom {
-    int y0, y1;   // valid rows [y0, y1)
-    int xs;       // first pixel of the segment (may be < 0)
+    int y0, y1;   // rows [y0, y1)
+    int xs;       // first pixel of the segment
     int j0, j1;   // bracketing block rows (clamped)
     int ic0, nc;  // first staged model column, number staged
 };
 
-__device__ __forceinline__ ApplyGeom apply_geom(const ApplyArgs& a, int ty, int sg)
+__device__ __forceinline__ ApplyGeom apply_geom(const ApplyArgs& a, int j, int sg)
 {
     ApplyGeom g;
-    const int off = (a.D / 2) % 8;
     const float invD = 1.0f / (float)a.D;
-    const int ya = ty * 8 - off;
-    g.y0 = max(ya, 0);
-    g.y1 = min(ya + 8, a.H);
-    g.xs = sg * kSeg - off;
-    const int x0 = max(g.xs, 0);
-    const int jb = (int)floorf(((float)g.y0 + 0.5f) * invD - 0.5f);
-    g.j0 = min(max(jb, 0), a.By - 1);
-    g.j1 = min(max(jb + 1, 0), a.By - 1);
-    g.ic0 = min(max((int)floorf(((float)x0 + 0.5f) * invD - 0.5f), 0), a.Bx - 1);
+    g.y0 = max(j * a.D - a.D / 2, 0);
+    g.y1 = min(j * a.D + a.D / 2, a.H);
+    g.xs = sg * kSeg;
+    g.j0 = min(max(j - 1, 0), a.By - 1);
+    g.j1 = min(j, a.By - 1);
+    g.ic0 = min(max((int)floorf(((float)g.xs + 0.5f) * invD - 0.5f), 0), a.Bx - 1);
     g.nc = min(kApplyNCol, a.Bx - g.ic0);
     return g;
 }
@@ -312,15 +325,15 @@ __device__ __forceinline__ void apply_consume(Ring& r, Seq& sq, const ApplyArgs&
     const ApplyGeom g = apply_geom(a, ty, sg);
     const float invD = 1.0f / (float)a.D;
     {  // models: copy out of the ring so the stage can be refilled at once
-        const float* st = ring_wait(r);
+        const float* st = ring_wait(r, sq, lane);
         const float4* s4 = reinterpret_cast<const float4*>(st);
         float4* d4 = reinterpret_cast<float4*>(mod);
         for (int i = lane; i < 2 * kApplyNCol * MS / 4; i += 32) d4[i] = s4[i];
         ring_release(r, sq, lane);
     }
     const int xq = g.xs + lane * 4;  // the lane's quad
-    const bool active = xq >= 0 && xq < a.W;
-    const float fxq = ((float)max(xq, 0) + 0.5f) * invD - 0.5f;
+    const bool active = xq < a.W;
+    const float fxq = ((float)xq + 0.5f) * invD - 0.5f;
     const int ib = (int)floorf(fxq);
     const int c0 = min(max(ib, 0), a.Bx - 1) - g.ic0;
     const int c1 = min(max(ib + 1, 0), a.Bx - 1) - g.ic0;
@@ -343,7 +356,7 @@ __device__ __forceinline__ void apply_consume(Ring& r, Seq& sq, const ApplyArgs&
                             fmaf(tyy, q.w - p.w, p.w));
         }
         __syncwarp();
-        const float* st = ring_wait(r);
+        const float* st = ring_wait(r, sq, lane);
         float gq[Q][4];
 #pragma unroll
         for (int j = 0; j < Q; ++j) {

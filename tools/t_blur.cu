@@ -7,6 +7,9 @@
 #include "../paper_2410_11625_b200/csrc/flr_tiles.cuh"
 
 using namespace flr;
+namespace flr {
+__device__ long long g_flr_dbg_times[64];
+}
 #define CK(x)                                                                              \
     do {                                                                                   \
         cudaError_t e = (x);                                                               \
@@ -52,17 +55,34 @@ int main(int argc, char** argv)
     CK(cudaMemcpy(mom, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
     CUtensorMap tm;
     bool ok = make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * KM, halo_x(R),
-                           kTileTY + 2 * R, kTileG);
+                           kTileTY + 2 * R, tile_g(R));
     printf("tmap ok=%d Bx=%d By=%d Bxp=%d\n", ok, Bx, By, Bxp);
     Taps t{};
     t.R = R;
     for (int i = -R; i <= R; ++i) t.g[R + i] = std::exp(-(double)(i * i) / (2.0 * 1.25 * 1.25));
     const size_t sm = blur_solve_smem_bytes(R);
     CK(cudaFuncSetAttribute(k_blur_solve<Q, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_blur_solve<Q, R><<<dim3(cdiv(Bx, kTileTX), cdiv(By, kTileTY), n), kTileTX * kTileTY, sm>>>(
-        tm, Bx, By, models, 28, 1e-5, 1e-4, t);
-    CK(cudaGetLastError());
-    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float ms = 0;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        k_blur_solve<Q, R><<<dim3(cdiv(Bx, kTileTX), cdiv(By, kTileTY), n), kTileTX * kTileTY, sm>>>(
+            tm, Bx, By, models, 28, 1e-5, 1e-4, t);
+        cudaEventRecord(e1);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        cudaEventElapsedTime(&ms, e0, e1);
+    }
+    printf("k_blur_solve %dx%d blocks: %.1f us\n", Bx, By, ms * 1e3);
+#ifdef FLR_DBG_TIMES
+    long long ht[64];
+    cudaMemcpyFromSymbol(ht, g_flr_dbg_times, sizeof(ht));
+    printf("tile phases (cycles from start):");
+    for (int i = 0; i < ht[63]; ++i) printf(" %lld", ht[i]);
+    printf("\n");
+#endif
     std::vector<float> m((size_t)Bx * By * 28);
     CK(cudaMemcpy(m.data(), models, m.size() * 4, cudaMemcpyDeviceToHost));
     printf("model[0] = %g %g %g\n", m[0], m[1], m[2]);

@@ -53,7 +53,7 @@ int main()
     ApplyArgs aa;
     make_tmap_3d(&aa.tg, G, W, H, NF * Q, kSeg, Q);
     aa.models = M, aa.out = O, aa.W = W, aa.H = H, aa.D = D, aa.Bx = Bx, aa.By = By;
-    aa.nseg = (W + 4 + kSeg - 1) / kSeg, aa.ntile = (H + 4 + 7) / 8;
+    aa.nseg = (W + kSeg - 1) / kSeg, aa.nband = apply_nband(H, D, By);
     using AC = ApplyCfg<Q>;
     cudaFuncSetAttribute(k_apply_stream<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AC::SMEM);
     for (int nf : {1, 4}) {
