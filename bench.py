@@ -290,15 +290,17 @@ def run_flr(args, cfg, rank, world, local_rank):
     R = flr.effective_radius(block=D, upsample=U, sigma=sigma)
 
     # ---- inputs resident in HBM (global frame index -> seed; ranks draw disjoint frames)
-    base_seed = 1000 + rank * pool * F
+    from paper_2410_11625_b200 import dist as fd
+
+    seeds = fd.frame_seeds(rank, world, pool * F)
     gl, yl, gh = [], [], []
     for i in range(pool):
         if U == 1:
-            g, y = synth.batch(F, W, H, Q=Q, seed0=base_seed + i * F, device=dev)
+            g, y = synth.batch(F, W, H, Q=Q, seed0=seeds[i * F], device=dev)
             gl.append(g)
             yl.append(y)
         else:
-            trip = [synth.upsample_pair(W, H, U=U, Q=Q, seed=base_seed + i * F + j, device=dev) for j in range(F)]
+            trip = [synth.upsample_pair(W, H, U=U, Q=Q, seed=seeds[i * F + j], device=dev) for j in range(F)]
             gl.append(torch.stack([t[0] for t in trip]).contiguous())
             yl.append(torch.stack([t[1] for t in trip]).contiguous())
             gh.append(torch.stack([t[2] for t in trip]).contiguous())
@@ -407,10 +409,7 @@ def run_flr(args, cfg, rank, world, local_rank):
             per_kernel[names[j]].append(evs[j].elapsed_time(evs[j + 1]))
     avg_ms = {n: (sum(v) / len(v) if v else None) for n, v in per_kernel.items()}
 
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = fd.max_over_ranks(ms, device=dev)
 
     # ---- end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
     E = max(1, args.e2e_steps)
@@ -446,23 +445,14 @@ def run_flr(args, cfg, rank, world, local_rank):
             e2e_step(i)
         b.record(stream)
         torch.cuda.synchronize()
-        e_ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e_ms = float(e_ms.item())
+        e_ms = fd.max_over_ranks(a.elapsed_time(b), device=dev)
         e2e = {"value": world * E * F * out_pixels(cfg) / (e_ms * 1e-3) / 1e6, "unit": "Mpixel/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / E, "steps": E}
 
     # ---- checksums of one output per rank, gathered over NCCL (the only collective)
     o = call(0)
     torch.cuda.synchronize()
-    cs = torch.tensor([float(o.double().sum()), float(o.double().abs().max()),
-                       float(torch.isfinite(o).all())], dtype=torch.float64, device=dev)
-    if world > 1:
-        allcs = [torch.empty_like(cs) for _ in range(world)]
-        dist.all_gather(allcs, cs)
-    else:
-        allcs = [cs]
+    allcs = fd.gather_rows(fd.output_checksum(o), device=dev)
 
     if rank != 0:
         return
@@ -509,7 +499,7 @@ def run_flr(args, cfg, rank, world, local_rank):
         "kernel_us": {n: (t * 1e3 if t else None) for n, t in avg_ms.items()},
         "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": launches_per_step * K,
         "clocks": clocks,
-        "checksums": [[float(v) for v in c.tolist()] for c in allcs],
+        "checksums": allcs,
         "paper_context": {"rtx2080ti_ms_per_1080p_frame": 0.636, "source": "P:429 (Table 1)"},
     }
     if check is not None:

@@ -70,7 +70,7 @@ typedef enum {
 /* Kernel schedule.  All variants compute the same result within the parity
  * bar; AUTO picks the fastest one for the shape. */
 typedef enum {
-    FLR_VARIANT_AUTO = 0,   /* FUSED when compiled for the shape, else STAGED */
+    FLR_VARIANT_AUTO = 0,   /* the fastest schedule for the shape (currently STAGED) */
     FLR_VARIANT_STAGED = 1, /* moments -> blur+solve -> apply, one launch each */
     FLR_VARIANT_FUSED = 2   /* one persistent warp-specialised kernel (row wavefront);
                                FLR_ERR_UNSUPPORTED when not compiled for the shape */

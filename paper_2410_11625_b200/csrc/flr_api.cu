@@ -271,7 +271,9 @@ flr_status flr_denoise_upsample_traced(int32_t n, int32_t Q, int32_t W_lo, int32
     float* models = (float*)((char*)workspace + L.models);
     const int ms = mstride_of(Q);
     LaunchCtx ctx = make_ctx(stream, trace);
-    if (p->variant != FLR_VARIANT_STAGED) {
+    // AUTO currently resolves to STAGED: on B200 the fused wavefront kernel is still
+    // solver-bound; it is selected explicitly with FUSED.
+    if (p->variant == FLR_VARIANT_FUSED) {
         FusedLaunch F;
         F.n = n, F.W = W_lo, F.H = H_lo, F.D = D, F.U = p->upsample, F.Bx = Bx, F.By = By;
         F.G = guides_lo, F.Y = radiance_lo, F.Gout = guides_hi, F.out = out;

@@ -139,6 +139,7 @@ __device__ __forceinline__ void fit_consume(Ring& r, Seq& q, const FitArgs& a, i
         for (int p = 0; p < QP; ++p) XY2[cc][p] = 0ull;
     }
 
+#pragma unroll 1  // keep the row body resident in the instruction cache
     for (int rr = 0; rr < rows; ++rr) {
         const float* st = ring_wait(r, q, lane);
         if (rr == 0) {
@@ -344,6 +345,7 @@ __device__ __forceinline__ void apply_consume(Ring& r, Seq& sq, const ApplyArgs&
                     ((float)(xq + 2 * h + 1) + 0.5f) * invD - 0.5f - (float)ib);
     const size_t plane = (size_t)a.W * a.H;
     float* O = a.out + (size_t)f * 3 * plane;
+#pragma unroll 1
     for (int y = g.y0; y < g.y1; ++y) {
         const float fy = ((float)y + 0.5f) * invD - 0.5f;
         const float tyy = fy - floorf(fy);

@@ -33,9 +33,9 @@ int main()
     cudaEventCreate(&e1);
 
     FitArgs fa;
-    make_tmap_3d(&fa.tg, G, W, H, NF * Q, kSeg, Q);
-    make_tmap_3d(&fa.ty, Y, W, H, NF * 3, kSeg, 3);
-    fa.mom = mom, fa.W = W, fa.H = H, fa.Bx = Bx, fa.By = By, fa.nseg = W / kSeg;
+    make_tmap_planes(&fa.tg, G, W, H, NF * Q, kSeg, Q);
+    make_tmap_planes(&fa.ty, Y, W, H, NF * 3, kSeg, 3);
+    fa.mom = mom, fa.W = W, fa.H = H, fa.Bx = Bx, fa.Bxp = mom_pitch(Bx), fa.By = By, fa.nseg = W / kSeg;
     using FC = FitCfg<Q>;
     cudaFuncSetAttribute(k_fit_stream<Q, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM);
     float ms = 0;
@@ -51,7 +51,7 @@ int main()
                plane * (Q + 3) * 4.0 * nf / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     }
     ApplyArgs aa;
-    make_tmap_3d(&aa.tg, G, W, H, NF * Q, kSeg, Q);
+    make_tmap_planes(&aa.tg, G, W, H, NF * Q, kSeg, Q);
     aa.models = M, aa.out = O, aa.W = W, aa.H = H, aa.D = D, aa.Bx = Bx, aa.By = By;
     aa.nseg = (W + kSeg - 1) / kSeg, aa.nband = apply_nband(H, D, By);
     using AC = ApplyCfg<Q>;
