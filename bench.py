@@ -90,6 +90,7 @@ KERNEL_BYTES = {
     # algorithmic bytes per frame of each launch: the full-resolution planes it must read + write
     "k_fit_moments": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
     "k_fit_stream": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
+    "k_fit_ldg": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
     "k_apply_stream": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
     "k_apply_tile": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
     "k_apply_px": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),

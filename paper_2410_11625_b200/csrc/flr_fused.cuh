@@ -209,8 +209,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_flr_fused(const __grid_con
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
             }
             gs.sync();
+#ifndef FLR_DBG_FAKE_SOLVE
             blur_solve_tile<Q, R>(&a.tmom, f, cx * kTileTX, m * kTileTY, a.fit.Bx, By, const_cast<float*>(a.app.models),
                                   SD::MS, a.eps_add, a.eps_mul, a.taps, sm, sbar, use, tid, gs);
+#endif
             __threadfence();
             gs.sync();
             if (tid == 0) red_release_add(&a.solve_done[f * a.nrt + m], 1);

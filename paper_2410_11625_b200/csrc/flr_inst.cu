@@ -71,6 +71,14 @@ template <int Q, int D>
 static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
                       cudaStream_t s)
 {
+    static const bool use_tma = std::getenv("FLR_FIT_TMA") != nullptr;
+    if (!use_tma && vec_ok(G, W) && vec_ok(Y, W)) {  // default: LDG-prefetch persistent kernel
+        FitLdgArgs la{G, Y, mom, W, H, Bx, mom_pitch(Bx), By, cdiv(W, kSeg)};
+        const int items = n * By * la.nseg;
+        const int grid = min(num_sms(), cdiv(items, kFitLdgWarps));
+        launch_pdl(k_fit_ldg<Q, D>, dim3(grid), dim3(kFitLdgWarps * 32), 0, s, la, n);
+        return;
+    }
     FitArgs a;
     if (vec_ok(G, W) && vec_ok(Y, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q) &&
         make_tmap_planes(&a.ty, Y, W, H, n * 3, kSeg, 3)) {  // TMA-fed persistent path
@@ -103,7 +111,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     const cudaStream_t s = ctx.s;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
-        ctx.before(vec_ok(G, W) && vec_ok(Y, W) ? "k_fit_stream" : "k_fit_moments");
+        ctx.before(!vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_TMA") ? "k_fit_stream" : "k_fit_ldg");
         if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s);
         else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s);
         else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s);
@@ -118,7 +126,10 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     CUtensorMap tm;
     const int Bxp = mom_pitch(Bx), R = taps.R;
     constexpr int NGRP = (Dims<Q>::KM + kBlurG - 1) / kBlurG;
-    if (R >= 1 && R <= kTileMaxR && !std::getenv("FLR_TILE_SOLVE") &&
+    // default: the tile kernel (blur + solve per 32x4 tile, no blurred-field round trip
+    // through L2/HBM); FLR_SPLIT_SOLVE selects the component-parallel blur + per-block solve
+    static const bool split = std::getenv("FLR_SPLIT_SOLVE") != nullptr;
+    if (split && R >= 1 && R <= kTileMaxR &&
         make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, blur_halo_x(R),
                      kBlurTY + 2 * R, kBlurG)) {
         ctx.before("k_blur");
@@ -142,7 +153,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
 #define FLR_K2(RR)                                                                                  \
     case RR:                                                                                        \
         set_smem(k_blur_solve<Q, RR>, sm);                                                          \
-        k_blur_solve<Q, RR><<<grid, block, sm, s>>>(tm, Bx, By, models, mstride, ea, em, taps);      \
+        launch_pdl(k_blur_solve<Q, RR>, grid, block, sm, s, tm, Bx, By, models, mstride, ea, em, taps); \
         break;
         switch (taps.R) { FLR_K2(1) FLR_K2(2) FLR_K2(3) FLR_K2(4) FLR_K2(5) FLR_K2(6) FLR_K2(7) FLR_K2(8) }
 #undef FLR_K2

@@ -9,6 +9,16 @@
 
 namespace flr {
 
+// L2 policy of the fit pass's guide reads (FLR_FIT_GUIDES_EVICT_LAST builds keep them resident)
+__device__ __forceinline__ uint64_t std_policy_guides_fit()
+{
+#ifdef FLR_FIT_GUIDES_NORMAL
+    return policy_evict_normal();
+#else
+    return policy_evict_last();
+#endif
+}
+
 // ring geometry of a streaming kernel: S stages of STG floats + EXTRA floats per warp
 template <int STG_, int EXTRA_, int S_, int MAXW>
 struct RingCfg {
@@ -54,20 +64,30 @@ struct RingSmem {
     }
 };
 
-// producer cursor over a warp's FIT items: one stage per pixel row
+// producer cursor over a warp's FIT items: one stage per pixel row (item decoded once)
 template <int Q, int D>
 struct FitSeq {
     const FitArgs* a;
-    int it, row, nitems, per_frame, step;
+    int it, nitems, per_frame, step;
+    int f, by, sg, row, rows;
     uint64_t pg, py;
+    __device__ void decode()
+    {
+        row = 0;
+        if (it >= nitems) return;
+        f = it / per_frame;
+        const int rem = it - f * per_frame;
+        by = rem / a->nseg;
+        sg = rem - by * a->nseg;
+        rows = min(D, a->H - by * D);
+    }
     __device__ bool next(float* dst, uint64_t* bar)
     {
         if (it >= nitems) return false;
-        const int f = it / per_frame, rem = it % per_frame, by = rem / a->nseg, sg = rem % a->nseg;
         fit_issue_row<Q, D>(*a, f, by, sg, row, dst, bar, pg, py);
-        if (++row == min(D, a->H - by * D)) {
-            row = 0;
+        if (++row == rows) {
             it += step;
+            decode();
         }
         return true;
     }
@@ -77,22 +97,31 @@ struct FitSeq {
 template <int Q>
 struct ApplySeq {
     const ApplyArgs* a;
-    int it, row, nitems, per_frame, step;
+    int it, nitems, per_frame, step;
+    int f, row;
+    ApplyGeom g;
     uint64_t pg, pm;
+    __device__ void decode()
+    {
+        row = -1;
+        if (it >= nitems) return;
+        f = it / per_frame;
+        const int rem = it - f * per_frame;
+        g = apply_geom(*a, rem / a->nseg, rem % a->nseg);
+    }
     __device__ bool next(float* dst, uint64_t* bar)
     {
         if (it >= nitems) return false;
-        const int f = it / per_frame, rem = it % per_frame;
-        const ApplyGeom g = apply_geom(*a, rem / a->nseg, rem % a->nseg);
         if (row < 0) {
             apply_issue_models<Q>(*a, g, f, dst, bar, pm);
             row = g.y0;
         } else {
             apply_issue_row<Q>(*a, g, f, row, dst, bar, pg);
-            if (++row == g.y1) {
-                row = -1;
-                it += step;
-            }
+            ++row;
+        }
+        if (row >= g.y1) {
+            it += step;
+            decode();
         }
         return true;
     }
@@ -110,13 +139,52 @@ __global__ void __launch_bounds__(FitCfg<Q>::THREADS, 1) k_fit_stream(const __gr
     const int per_frame = a.By * a.nseg, nitems = n * per_frame;
     const int GW = gridDim.x * C::NSW, first = blockIdx.x * C::NSW + w;
     Ring r = sm.ring(w);
-    FitSeq<Q, D> seq{&a, first, 0, nitems, per_frame, GW, policy_evict_normal(), policy_evict_first()};
+    FitSeq<Q, D> seq;
+    seq.a = &a, seq.it = first, seq.nitems = nitems, seq.per_frame = per_frame, seq.step = GW;
+    // guides are read again by the apply pass: keep them in L2; radiance is read once
+    seq.pg = std_policy_guides_fit(), seq.py = policy_evict_first();
+    seq.decode();
     pdl_trigger();
     pdl_wait();  // caller data may come from the previous grid: wait before the first read
     if (lane == 0) ring_fill(r, seq);
+#ifdef FLR_DBG_TIMES
+    const long long tk0 = clock64();
+    int nit = 0;
+#endif
     for (int it = first; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it % per_frame;
         fit_consume<Q, D>(r, seq, a, f, rem / a.nseg, rem % a.nseg, lane);
+#ifdef FLR_DBG_TIMES
+        ++nit;
+#endif
+    }
+#ifdef FLR_DBG_TIMES
+    extern __device__ unsigned long long g_flr_total_cycles[4096];
+    extern __device__ int g_flr_items[4096];
+    if (lane == 0) {
+        g_flr_total_cycles[(blockIdx.x * 32 + w) & 4095] = clock64() - tk0;
+        g_flr_items[(blockIdx.x * 32 + w) & 4095] = nit;
+    }
+#endif
+}
+
+#ifndef FLR_FITLDG_WARPS
+#define FLR_FITLDG_WARPS 8
+#endif
+constexpr int kFitLdgWarps = FLR_FITLDG_WARPS;
+
+// K1 without shared memory: persistent, one warp per FIT item, LDG prefetch of the next row
+template <int Q, int D>
+__global__ void __launch_bounds__(kFitLdgWarps * 32, 1) k_fit_ldg(const __grid_constant__ FitLdgArgs a, int n)
+{
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int per_frame = a.By * a.nseg, nitems = n * per_frame;
+    const int GW = gridDim.x * kFitLdgWarps;
+    pdl_trigger();
+    pdl_wait();
+    for (int it = blockIdx.x * kFitLdgWarps + w; it < nitems; it += GW) {
+        const int f = it / per_frame, rem = it - f * per_frame, by = rem / a.nseg;
+        fit_ldg_item<Q, D>(a, f, by, rem - by * a.nseg, lane);
     }
 }
 
@@ -132,7 +200,10 @@ __global__ void __launch_bounds__(ApplyCfg<Q>::THREADS, 1) k_apply_stream(const 
     const int per_frame = a.nband * a.nseg, nitems = n * per_frame;
     const int GW = gridDim.x * C::NSW, first = blockIdx.x * C::NSW + w;
     Ring r = sm.ring(w);
-    ApplySeq<Q> seq{&a, first, -1, nitems, per_frame, GW, policy_evict_first(), policy_evict_normal()};
+    ApplySeq<Q> seq;
+    seq.a = &a, seq.it = first, seq.nitems = nitems, seq.per_frame = per_frame, seq.step = GW;
+    seq.pg = policy_evict_first(), seq.pm = policy_evict_normal();  // last use of the guides
+    seq.decode();
     pdl_trigger();
     pdl_wait();  // models come from the previous grid
     if (lane == 0) ring_fill(r, seq);

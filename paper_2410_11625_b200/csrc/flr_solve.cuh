@@ -19,10 +19,23 @@
 
 namespace flr {
 
+// storage of the normalised right-hand sides B^[i][c] (registers or shared memory)
+template <int Q>
+struct RegB {
+    double b[Q][3];
+    __device__ __forceinline__ double& operator()(int i, int c) { return b[i][c]; }
+};
+struct SmemB {
+    double* p;   // element (i, c) at p[(3 i + c) * stride]
+    int stride;
+    __device__ __forceinline__ double& operator()(int i, int c) { return p[(3 * i + c) * stride]; }
+};
+
 // `m(k)` returns the blurred fp64 moment component k (layout of flr_common.cuh).
-// Writes 3(Q+1) floats to `out` (row 0 = bias).
-template <int Q, class MomentFn>
-__device__ __forceinline__ void solve_block(MomentFn&& m, double eps_add, double eps_mul, float* out)
+// Writes 3(Q+1) floats to `out` (row 0 = bias).  The 3 right-hand sides are solved one
+// channel at a time so the live set stays small (B may live in shared memory).
+template <int Q, class MomentFn, class BStore>
+__device__ __forceinline__ void solve_block_b(MomentFn&& m, double eps_add, double eps_mul, float* out, BStore& B)
 {
     using Dm = Dims<Q>;
     const double n = m(Dm::C_N);
@@ -46,11 +59,10 @@ __device__ __forceinline__ void solve_block(MomentFn&& m, double eps_add, double
     double muY[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) muY[c] = m(Dm::C_Y + c) * inv_n;
-    double B[Q][3];
 #pragma unroll
     for (int i = 0; i < Q; ++i)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) B[i][c] = fma(m(Dm::C_XY + i * 3 + c), inv_n, -mu[i] * muY[c]) * isig[i];
+        for (int c = 0; c < 3; ++c) B(i, c) = fma(m(Dm::C_XY + i * 3 + c), inv_n, -mu[i] * muY[c]) * isig[i];
     // C^ + eps I in place (upper triangle)
 #pragma unroll
     for (int i = 0; i < Q; ++i)
@@ -80,42 +92,44 @@ __device__ __forceinline__ void solve_block(MomentFn&& m, double eps_add, double
             Wh[Dm::s_idx(k, j) - Dm::C_S] = v * rinv[k];
         });
     });
-    // R^T z = B, then R A^ = z
-    static_for<Q>([&](auto K) {
-        constexpr int k = decltype(K)::value;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            double v = B[k][c];
+    // per channel: R^T z = B, R A^ = z, raw model column
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) {
+        double z[Q];
+        static_for<Q>([&](auto K) {
+            constexpr int k = decltype(K)::value;
+            double v = B(k, c);
             static_for<k>([&](auto PP) {
                 constexpr int p = decltype(PP)::value;
-                v = fma(-Wh[Dm::s_idx(p, k) - Dm::C_S], B[p][c], v);
+                v = fma(-Wh[Dm::s_idx(p, k) - Dm::C_S], z[p], v);
             });
-            B[k][c] = v * rinv[k];
-        }
-    });
-    static_for<Q>([&](auto KK) {
-        constexpr int k = Q - 1 - decltype(KK)::value;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            double v = B[k][c];
+            z[k] = v * rinv[k];
+        });
+        static_for<Q>([&](auto KK) {
+            constexpr int k = Q - 1 - decltype(KK)::value;
+            double v = z[k];
             static_for<Q - 1 - k>([&](auto PP) {
                 constexpr int p = k + 1 + decltype(PP)::value;
-                v = fma(-Wh[Dm::s_idx(k, p) - Dm::C_S], B[p][c], v);
+                v = fma(-Wh[Dm::s_idx(k, p) - Dm::C_S], z[p], v);
             });
-            B[k][c] = v * rinv[k];
-        }
-    });
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
+            z[k] = v * rinv[k];
+        });
         double bias = muY[c];
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
-            const double a = B[j][c] * isig[j];
+            const double a = z[j] * isig[j];
             out[(1 + j) * 3 + c] = (float)a;
             bias = fma(-mu[j], a, bias);
         }
         out[c] = (float)bias;
     }
+}
+
+template <int Q, class MomentFn>
+__device__ __forceinline__ void solve_block(MomentFn&& m, double eps_add, double eps_mul, float* out)
+{
+    RegB<Q> B;
+    solve_block_b<Q>(m, eps_add, eps_mul, out, B);
 }
 
 }  // namespace flr

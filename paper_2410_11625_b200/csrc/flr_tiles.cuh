@@ -410,6 +410,8 @@ __global__ void __launch_bounds__(kTileTX* kTileTY) k_blur_solve(const __grid_co
         mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
+    pdl_trigger();
+    pdl_wait();  // the moment field comes from the previous grid
     __syncthreads();
     unsigned use[2] = {0, 0};
     blur_solve_tile<Q, R>(&tm, blockIdx.z, blockIdx.x * kTileTX, blockIdx.y * kTileTY, Bx, By, models, mstride,

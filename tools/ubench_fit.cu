@@ -7,6 +7,13 @@
 #include "../paper_2410_11625_b200/csrc/flr_persist.cuh"
 
 using namespace flr;
+#ifdef FLR_DBG_TIMES
+namespace flr {
+__device__ unsigned long long g_flr_wait_cycles[4096];
+__device__ unsigned long long g_flr_total_cycles[4096];
+__device__ int g_flr_items[4096];
+}
+#endif
 
 int main()
 {
@@ -49,6 +56,44 @@ int main()
         }
         printf("fit   nf=%d warps=%d S=%d: %7.1f us/frame  %6.0f GB/s (%s)\n", nf, FC::NSW, FC::S, 1e3 * ms / nf,
                plane * (Q + 3) * 4.0 * nf / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+#ifdef FLR_DBG_TIMES
+        {
+            static unsigned long long w[4096], tt[4096];
+            static int it[4096];
+            cudaMemset(g_flr_wait_cycles, 0, 0);
+            unsigned long long zero[4096] = {};
+            cudaMemcpyToSymbol(g_flr_wait_cycles, zero, sizeof(zero));
+            k_fit_stream<Q, D><<<sms, FC::THREADS, FC::SMEM>>>(fa, nf);
+            cudaDeviceSynchronize();
+            cudaMemcpyFromSymbol(w, g_flr_wait_cycles, sizeof(w));
+            cudaMemcpyFromSymbol(tt, g_flr_total_cycles, sizeof(tt));
+            cudaMemcpyFromSymbol(it, g_flr_items, sizeof(it));
+            double sw = 0, st = 0, mx = 0; int n = 0, hist[8] = {};
+            for (int b = 0; b < sms; ++b)
+                for (int ww = 0; ww < FC::NSW; ++ww) {
+                    const int i = b * 32 + ww;
+                    sw += w[i]; st += tt[i]; ++n; if (tt[i] > mx) mx = tt[i]; hist[it[i] < 8 ? it[i] : 7]++;
+                }
+            printf("   per-warp: mean total %.0f cyc, mean wait %.0f cyc (%.0f%%), max total %.0f; items/warp hist:",
+                   st / n, sw / n, 100 * sw / st, mx);
+            for (int k = 0; k < 8; ++k) printf(" %d", hist[k]);
+            printf("\n");
+        }
+#endif
+    }
+    {
+        FitLdgArgs la{G, Y, mom, W, H, Bx, mom_pitch(Bx), By, W / kSeg};
+        for (int nf : {1, 4}) {
+            for (int rep = 0; rep < 5; ++rep) {
+                cudaEventRecord(e0);
+                k_fit_ldg<Q, D><<<sms, kFitLdgWarps * 32>>>(la, nf);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                cudaEventElapsedTime(&ms, e0, e1);
+            }
+            printf("fitldg nf=%d warps=%d: %7.1f us/frame  %6.0f GB/s (%s)\n", nf, kFitLdgWarps, 1e3 * ms / nf,
+                   plane * (Q + 3) * 4.0 * nf / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+        }
     }
     ApplyArgs aa;
     make_tmap_planes(&aa.tg, G, W, H, NF * Q, kSeg, Q);
