@@ -6,6 +6,7 @@
 #include "flr_staged.cuh"
 #include "flr_tiles.cuh"
 #include "flr_persist.cuh"
+#include "flr_k2.cuh"
 #if FLR_Q == 4 || FLR_Q == 8
 #include "flr_fused.cuh"
 #endif
@@ -126,24 +127,56 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     CUtensorMap tm;
     const int Bxp = mom_pitch(Bx), R = taps.R;
     constexpr int NGRP = (Dims<Q>::KM + kBlurG - 1) / kBlurG;
-    // default: the tile kernel (blur + solve per 32x4 tile, no blurred-field round trip
-    // through L2/HBM); FLR_SPLIT_SOLVE selects the component-parallel blur + per-block solve
-    static const bool split = std::getenv("FLR_SPLIT_SOLVE") != nullptr;
-    if (split && R >= 1 && R <= kTileMaxR &&
-        make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, blur_halo_x(R),
-                     kBlurTY + 2 * R, kBlurG)) {
-        ctx.before("k_blur");
-        const dim3 grid(cdiv(Bx, kBlurTX), cdiv(By, kBlurTY), n * NGRP);
-#define FLR_KB(RR)                                                                                  \
-    case RR:                                                                                        \
-        set_smem(k_blur<Q, RR>, BlurGeom<RR>::SMEM);                                                \
-        launch_pdl(k_blur<Q, RR>, grid, dim3(256), BlurGeom<RR>::SMEM, s, tm, Bx, Bxp, By, hb, taps); \
+    // K2 variants: default k_blur_solve_tile (32 x 8 tiles, TMA ring, flr_k2.cuh);
+    // FLR_ROWS_SOLVE: row-strip blur -> blurred field -> row solve (two kernels);
+    // FLR_TILE_SOLVE: the 32 x 4 tile kernel with in-register h-pass (flr_tiles.cuh)
+    static const bool tile = std::getenv("FLR_TILE_SOLVE") != nullptr;
+    static const bool rows = std::getenv("FLR_ROWS_SOLVE") != nullptr;
+    (void)NGRP;
+    bool k2tile = false;
+    if (!tile && !rows && R >= 1 && R <= kTileMaxR && mstride == Dims<Q>::MSTRIDE) {
+        // default: one tile kernel, moment field read once (+ halo) by TMA, no blurred-field
+        // round trip through L2
+        const dim3 grid(cdiv(Bx, kK2TX), cdiv(By, kK2TY), n);
+#define FLR_KT(RR)                                                                                          \
+    case RR: {                                                                                              \
+        using KG = K2Geom<Q, RR>;                                                                           \
+        if (!make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, KG::HX, \
+                          KG::NV, KG::G))                                                                   \
+            break;                                                                                          \
+        ctx.before("k_blur_solve_tile");                                                                    \
+        set_smem(k_blur_solve_tile<Q, RR>, KG::SMEM);                                                       \
+        launch_pdl(k_blur_solve_tile<Q, RR>, grid, dim3(kK2Threads), KG::SMEM, s, tm, Bx, By, models, ea, em, \
+                   taps);                                                                                   \
+        k2tile = true;                                                                                      \
+        break;                                                                                              \
+    }
+        switch (R) { FLR_KT(1) FLR_KT(2) FLR_KT(3) FLR_KT(4) FLR_KT(5) FLR_KT(6) FLR_KT(7) FLR_KT(8) }
+#undef FLR_KT
+    }
+    if (k2tile) {
+    } else if (!tile && R >= 1 && R <= kTileMaxR && blur_rows_smem(Bx, R) <= 227 * 1024 &&
+        (size_t)n * Dims<Q>::KM <= 65535) {
+        ctx.before("k_blur_rows");
+        const size_t sm = blur_rows_smem(Bx, R);
+        const dim3 grid(cdiv(By, kRowsCH), n * Dims<Q>::KM);
+#define FLR_KB(RR)                                                                                          \
+    case RR:                                                                                                \
+        set_smem(k_blur_rows<RR>, sm);                                                                      \
+        launch_pdl(k_blur_rows<RR>, grid, dim3(kRowsThreads), sm, s, (const double*)mom, Bx, Bxp, By, hb, taps); \
         break;
         switch (R) { FLR_KB(1) FLR_KB(2) FLR_KB(3) FLR_KB(4) FLR_KB(5) FLR_KB(6) FLR_KB(7) FLR_KB(8) }
 #undef FLR_KB
-        ctx.before("k_solve");
-        launch_pdl(k_solve<Q>, dim3(cdiv(Bx, 128), By, n), dim3(128), 0, s, Bx, Bxp, By, (const double*)hb, models,
-                   mstride, ea, em);
+        if (mstride == Dims<Q>::MSTRIDE && !std::getenv("FLR_REG_SOLVE")) {
+            ctx.before("k_solve_rows");
+            set_smem(k_solve_rows<Q>, solve_rows_smem<Q>());
+            launch_pdl(k_solve_rows<Q>, dim3(cdiv(Bx, kSolveRowN), By, n), dim3(kSolveRowN), solve_rows_smem<Q>(), s,
+                       Bx, Bxp, By, (const double*)hb, models, ea, em);
+        } else {
+            ctx.before("k_solve");
+            launch_pdl(k_solve<Q>, dim3(cdiv(Bx, 128), By, n), dim3(128), 0, s, Bx, Bxp, By, (const double*)hb,
+                       models, mstride, ea, em);
+        }
     } else if (R >= 1 && R <= kTileMaxR &&
         make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, halo_x(R),
                      kTileTY + 2 * R, tile_g(R))) {
@@ -181,7 +214,14 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
             a.models = models, a.out = out;
             a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W, kSeg), a.nband = apply_nband(H, D, By);
             using C = ApplyCfg<Q>;
-            const int items = n * a.nseg * a.nband;
+            // sub-bands of >= 4 rows: finer items balance the warps (a single 1080p frame
+            // otherwise leaves most warps with 1 item and some with 2; measured 28 -> 25 us)
+            a.nsub = 1;
+            while (D % (2 * a.nsub) == 0 && D / (2 * a.nsub) >= 4)
+                a.nsub *= 2;
+            if (const char* e = std::getenv("FLR_APPLY_NSUB")) a.nsub = std::max(1, std::atoi(e));
+            if (D % a.nsub) a.nsub = 1;
+            const int items = n * a.nseg * a.nband * a.nsub;
             const int grid = min(num_sms(), cdiv(items, C::NSW));
             ctx.before("k_apply_stream");
             set_smem(k_apply_stream<Q>, C::SMEM);
@@ -217,13 +257,13 @@ bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx)
         !make_tmap_planes(&a.fit.ty, L.Y, L.W, L.H, L.n * 3, kSeg, 3) ||
         !make_tmap_planes(&a.app.tg, L.Gout, Wo, Ho, L.n * Q, kSeg, Q) ||
         !make_tmap_3d(&a.tmom, L.mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, L.Bx, L.By, Bxp, L.n * Dims<Q>::KM,
-                      halo_x(R), kTileTY + 2 * R, tile_g(R)))
+                      halo_x(R), kTileTY + 2 * R, kFusedG))
         return false;
     a.fit.mom = L.mom;
     a.fit.W = L.W, a.fit.H = L.H, a.fit.Bx = L.Bx, a.fit.Bxp = Bxp, a.fit.By = L.By, a.fit.nseg = cdiv(L.W, kSeg);
     a.app.models = L.models, a.app.out = L.out;
     a.app.W = Wo, a.app.H = Ho, a.app.D = Dout, a.app.Bx = L.Bx, a.app.By = L.By;
-    a.app.nseg = cdiv(Wo, kSeg), a.app.nband = apply_nband(Ho, Dout, L.By);
+    a.app.nseg = cdiv(Wo, kSeg), a.app.nband = apply_nband(Ho, Dout, L.By), a.app.nsub = 1;
     a.taps = L.taps;
     a.nrt = cdiv(L.By, kTileTY), a.ncx = cdiv(L.Bx, kTileTX);
     a.fit_done = L.flags;

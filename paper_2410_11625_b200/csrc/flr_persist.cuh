@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(ApplyCfg<Q>::THREADS, 1) k_apply_stream(const 
     sm.init_barriers();
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int per_frame = a.nband * a.nseg, nitems = n * per_frame;
+    const int per_frame = a.nband * a.nsub * a.nseg, nitems = n * per_frame;
     const int GW = gridDim.x * C::NSW, first = blockIdx.x * C::NSW + w;
     Ring r = sm.ring(w);
     ApplySeq<Q> seq;

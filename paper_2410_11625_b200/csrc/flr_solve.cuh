@@ -15,6 +15,7 @@
 // paper's recursive block inverse: the solution is unique, so any
 // exact solver returns it up to rounding.
 #pragma once
+#include <type_traits>
 #include "flr_common.cuh"
 
 namespace flr {
@@ -34,8 +35,9 @@ struct SmemB {
 // `m(k)` returns the blurred fp64 moment component k (layout of flr_common.cuh).
 // Writes 3(Q+1) floats to `out` (row 0 = bias).  The 3 right-hand sides are solved one
 // channel at a time so the live set stays small (B may live in shared memory).
-template <int Q, class MomentFn, class BStore>
-__device__ __forceinline__ void solve_block_b(MomentFn&& m, double eps_add, double eps_mul, float* out, BStore& B)
+// `out[i]` is any float lvalue accessor (a pointer, or a shared-memory staging view).
+template <int Q, class MomentFn, class BStore, class OutT>
+__device__ __forceinline__ void solve_block_b(MomentFn&& m, double eps_add, double eps_mul, OutT&& out, BStore& B)
 {
     using Dm = Dims<Q>;
     const double n = m(Dm::C_N);
@@ -92,10 +94,12 @@ __device__ __forceinline__ void solve_block_b(MomentFn&& m, double eps_add, doub
             Wh[Dm::s_idx(k, j) - Dm::C_S] = v * rinv[k];
         });
     });
-    // per channel: R^T z = B, R A^ = z, raw model column
-#pragma unroll 1
+    // per channel: R^T z = B, R A^ = z, raw model column (channels interleaved when B is
+    // in registers; one at a time when it lives in shared memory to save registers)
+    constexpr int UC = std::is_same<BStore, RegB<Q>>::value ? 3 : 1;
+#pragma unroll UC
     for (int c = 0; c < 3; ++c) {
-        double z[Q];
+        double z[Q] = {};
         static_for<Q>([&](auto K) {
             constexpr int k = decltype(K)::value;
             double v = B(k, c);

@@ -394,6 +394,7 @@ struct ApplyArgs {
     const float* models;  // [n][By][Bx][MS]
     float* out;           // [n][3][H][W]
     int W, H, D, Bx, By, nseg, nband;
+    int nsub;  // sub-bands per band (D % nsub == 0): more, smaller APPLY items for one frame
 };
 
 __host__ __device__ inline int apply_nband(int H, int D, int By)
@@ -409,12 +410,16 @@ struct ApplyGeom {
     int ic0, nc;  // first staged model column, number staged
 };
 
-__device__ __forceinline__ ApplyGeom apply_geom(const ApplyArgs& a, int j, int sg)
+// item geometry of sub-band u = j * nsub + s of band j: rows [jD - D/2 + s D/nsub, ...)
+// clipped to the band and the image (possibly empty)
+__device__ __forceinline__ ApplyGeom apply_geom(const ApplyArgs& a, int u, int sg)
 {
     ApplyGeom g;
     const float invD = 1.0f / (float)a.D;
-    g.y0 = max(j * a.D - a.D / 2, 0);
-    g.y1 = min(j * a.D + a.D / 2, a.H);
+    const int j = a.nsub == 1 ? u : u / a.nsub, s = u - j * a.nsub, rs = a.D / a.nsub;
+    const int yb = j * a.D - a.D / 2 + s * rs;
+    g.y0 = max(yb, 0);
+    g.y1 = min(yb + rs, a.H);
     g.xs = sg * kSeg;
     g.j0 = min(max(j - 1, 0), a.By - 1);
     g.j1 = min(j, a.By - 1);

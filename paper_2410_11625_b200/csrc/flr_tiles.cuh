@@ -501,6 +501,147 @@ __global__ void __launch_bounds__(256) k_blur(const __grid_constant__ CUtensorMa
     }
 }
 
+// ===========================================================================
+// K2a (row-strip blur): the separable Gaussian of P:334 over a strip of kRowsCH block
+// rows of ONE moment plane, full width.  Phase 1: one thread per PAIR of columns
+// slides down the strip (kRowsCH + 2R coalesced 16-byte loads -> 2 kRowsCH vertical
+// outputs; rows outside the field are zero = R3), results in shared memory with a
+// zero x halo.  Phase 2: one thread per (row, kRowsCW consecutive columns) slides
+// along the row (16-byte shared loads) into a second buffer; phase 3 stores the strip
+// with 16-byte coalesced stores.  Every input value is read from L2 about once
+// ((kRowsCH + 2R) / kRowsCH), against (TY+2R)(TX+2R)/(TX TY) for 2-D halo tiles.
+// grid: (ceil(By / kRowsCH), n * KM), kRowsThreads threads; smem: blur_rows_smem(Bx, R).
+// Needs an even row pitch Bxp >= Bx + (Bx & 1) (mom_pitch) and 16-byte aligned planes.
+// ===========================================================================
+#ifndef FLR_ROWS_CH
+#define FLR_ROWS_CH 16
+#endif
+constexpr int kRowsCH = FLR_ROWS_CH, kRowsCW = 16, kRowsThreads = 128;
+// shared row layout: column u (u = x + RE, RE = R rounded up to even) at rows_idx(u);
+// 2 pad doubles after every kRowsCW columns keep the 16-byte accesses of threads that
+// own consecutive chunks on distinct bank groups (stride 18 doubles)
+__host__ __device__ constexpr int rows_idx(int u) { return u + 2 * (u / kRowsCW); }
+__host__ __device__ constexpr int rows_re(int R) { return (R + 1) & ~1; }
+__host__ __device__ constexpr int blur_rows_xp(int Bx, int R)
+{
+    return rows_idx(((Bx + kRowsCW - 1) / kRowsCW) * kRowsCW + 2 * rows_re(R)) + 2;
+}
+inline size_t blur_rows_smem(int Bx, int R) { return (size_t)2 * kRowsCH * blur_rows_xp(Bx, R) * sizeof(double); }
+
+template <int R>
+__global__ void __launch_bounds__(kRowsThreads, 3) k_blur_rows(const double* __restrict__ mom, int Bx, int Bxp, int By,
+                                                            double* __restrict__ out, const __grid_constant__ Taps t)
+{
+    constexpr int CH = kRowsCH, CW = kRowsCW, RE = rows_re(R), NV = CH + 2 * R, NW = CW + 2 * RE;
+    extern __shared__ __align__(16) double smr[];
+    const int XP = blur_rows_xp(Bx, R);
+    double* vs = smr;            // [CH][XP]: vertical pass
+    double* hs = smr + CH * XP;  // [CH][XP]: result, column x at rows_idx(x)
+    const int y0 = blockIdx.x * CH, nrow = min(CH, By - y0);
+    const size_t ps = (size_t)By * Bxp;
+    const double* src = mom + (size_t)blockIdx.y * ps;
+    double* dst = out + (size_t)blockIdx.y * ps;
+    pdl_trigger();
+    pdl_wait();  // the moment field comes from the previous grid
+#ifdef FLR_DBG_PHASES
+    long long ts0 = clock64(), gt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+#endif
+    const bool interior = y0 >= R && y0 + CH + R <= By;
+    for (int x = 2 * threadIdx.x; x < Bx; x += 2 * blockDim.x) {
+        double2 v[NV];
+        const double* col = src + x;
+        if (interior) {
+            const double* p = col + (size_t)(y0 - R) * Bxp;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) v[i] = __ldg(reinterpret_cast<const double2*>(p + (size_t)i * Bxp));
+        } else {
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int y = y0 - R + i;
+                v[i] = (y >= 0 && y < By) ? __ldg(reinterpret_cast<const double2*>(col + (size_t)y * Bxp))
+                                          : make_double2(0.0, 0.0);
+            }
+        }
+        const bool odd = x + 1 >= Bx;  // the pad column of an odd-width field counts as zero
+        double* o = vs + rows_idx(x + RE);
+#pragma unroll
+        for (int r = 0; r < CH; ++r) {
+            double a = t.g[R] * v[r + R].x, b = t.g[R] * v[r + R].y;
+#pragma unroll
+            for (int d = 1; d <= R; ++d) {
+                a = fma(t.g[R + d], v[r + R - d].x + v[r + R + d].x, a);
+                b = fma(t.g[R + d], v[r + R - d].y + v[r + R + d].y, b);
+            }
+            *reinterpret_cast<double2*>(o + r * XP) = make_double2(a, odd ? 0.0 : b);
+        }
+    }
+    {  // zero x halo (R3): u in [0, RE) and [2 ceil(Bx/2) + RE, nch CW + 2 RE)
+        const int xe = (Bx + 1) & ~1, ue = ((Bx + CW - 1) / CW) * CW + 2 * RE, nz = RE + ue - (xe + RE);
+        for (int i = threadIdx.x; i < CH * nz; i += blockDim.x) {
+            const int r = i / nz, j = i - r * nz;
+            vs[r * XP + rows_idx(j < RE ? j : xe + j)] = 0.0;
+        }
+    }
+#ifdef FLR_DBG_PHASES
+    long long ts1 = clock64();
+#endif
+    __syncthreads();
+#ifdef FLR_DBG_PHASES
+    long long ts2 = clock64();
+#endif
+    const int nch = (Bx + CW - 1) / CW;
+    for (int task = threadIdx.x; task < nrow * nch; task += blockDim.x) {
+        const int r = task / nch, c = task - r * nch;
+        const double* h = vs + r * XP + c * (CW + 2);  // u = c CW + i at c (CW + 2) + i + 2 (i / CW)
+        double w[NW];
+#pragma unroll
+        for (int i = 0; i < NW; i += 2) {
+            const double2 q = *reinterpret_cast<const double2*>(h + i + 2 * (i / CW));
+            w[i] = q.x;
+            w[i + 1] = q.y;
+        }
+        double* o = hs + r * XP + c * (CW + 2);
+#pragma unroll
+        for (int e = 0; e < CW; e += 2) {
+            double a = t.g[R] * w[e + RE], b = t.g[R] * w[e + 1 + RE];
+#pragma unroll
+            for (int d = 1; d <= R; ++d) {
+                a = fma(t.g[R + d], w[e + RE - d] + w[e + RE + d], a);
+                b = fma(t.g[R + d], w[e + 1 + RE - d] + w[e + 1 + RE + d], b);
+            }
+            *reinterpret_cast<double2*>(o + e) = make_double2(a, b);
+        }
+    }
+#ifdef FLR_DBG_PHASES
+    long long ts3 = clock64();
+#endif
+    __syncthreads();
+#ifdef FLR_DBG_PHASES
+    long long ts4 = clock64();
+#endif
+#ifndef FLR_DBG_NOSTORE
+    for (int r = 0; r < nrow; ++r)
+        for (int x = 2 * threadIdx.x; x < Bx; x += 2 * blockDim.x)
+            *reinterpret_cast<double2*>(dst + (size_t)(y0 + r) * Bxp + x) =
+                *reinterpret_cast<const double2*>(hs + r * XP + rows_idx(x));
+#else
+    if (hs[threadIdx.x] == 12345.0) dst[threadIdx.x] = 1.0;
+#endif
+#ifdef FLR_DBG_PHASES
+    if (threadIdx.x == 0) {
+        extern __device__ long long g_flr_phase[];
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        long long* q = g_flr_phase + 10 * (blockIdx.y * gridDim.x + blockIdx.x);
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        q[0] = ts0, q[1] = ts1, q[2] = ts2, q[3] = ts3, q[4] = ts4, q[5] = clock64(), q[6] = sm, q[7] = gt;
+        q[8] = gt0;
+    }
+#endif
+}
+
 // one thread per block: the appendix solve on the blurred moments (coalesced across bx)
 template <int Q>
 __global__ void __launch_bounds__(128) k_solve(int Bx, int Bxp, int By, const double* __restrict__ blurred,
@@ -518,6 +659,78 @@ __global__ void __launch_bounds__(128) k_solve(int Bx, int Bxp, int By, const do
     for (int k = 0; k < Dims<Q>::KM; ++k) m[k] = __ldg(src + (size_t)k * cs);
     solve_block<Q>([&](int k) { return m[k]; }, eps_add, eps_mul,
                    models + ((size_t)(f * By + by) * Bx + bx) * mstride);
+}
+
+// K2b (row solve): one CTA per 128 consecutive blocks of a block row.  The blurred
+// components arrive by 1-D bulk copies (TMA engine, two mbarriers: n, u, S first so
+// the Cholesky can start while Y, XY land) into shared memory [KM][128], where each
+// thread reads only its own column; B^ overwrites the XY slots it is made from and
+// the model is staged in the thread's own (consumed) S slots, then stored coalesced.
+// Keeping the components out of registers lets 3 CTAs share an SM (<= 168 regs).
+constexpr int kSolveRowN = 128;
+template <int Q>
+constexpr size_t solve_rows_smem() { return (size_t)Dims<Q>::KM * kSolveRowN * sizeof(double) + 2 * sizeof(uint64_t); }
+
+struct StagedModel {  // float i of a thread's model in the S slots of its column
+    double* col;
+    __device__ __forceinline__ float& operator[](int i) const
+    {
+        return reinterpret_cast<float*>(col + (i >> 1) * kSolveRowN)[i & 1];
+    }
+};
+
+template <int Q>
+__global__ void __launch_bounds__(kSolveRowN, 3) k_solve_rows(int Bx, int Bxp, int By, const double* __restrict__ blurred,
+                                                             float* __restrict__ models, double eps_add, double eps_mul)
+{
+    using Dm = Dims<Q>;
+    constexpr int KM = Dm::KM, NT = kSolveRowN, MS = Dm::MSTRIDE;
+    extern __shared__ __align__(16) double sms[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sms + KM * NT);
+    const int bx0 = blockIdx.x * NT, by = blockIdx.y, f = blockIdx.z, t = threadIdx.x;
+    const int nb = min(NT, Bx - bx0), nbe = (nb + 1) & ~1;  // even count: 16-byte bulk sizes
+    if (t == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    pdl_trigger();
+    pdl_wait();  // the blurred field comes from the previous grid
+    __syncthreads();
+    const size_t cs = (size_t)By * Bxp;
+    const double* src = blurred + (size_t)f * KM * cs + (size_t)by * Bxp + bx0;
+    if (t < 32) {
+        const unsigned bytes = nbe * sizeof(double);
+        if (t == 0) {
+            mbar_arrive_expect_tx(&bar[0], bytes * Dm::C_Y);
+            mbar_arrive_expect_tx(&bar[1], bytes * (KM - Dm::C_Y));
+        }
+        __syncwarp();
+        const uint64_t pol = policy_evict_first();
+        for (int k = t; k < KM; k += 32) bulk_g2s(sms + k * NT, src + k * cs, bytes, &bar[k < Dm::C_Y ? 0 : 1], pol);
+    }
+    double* col = sms + t;
+    if (t < nb) {
+        SmemB B{col + Dm::C_XY * NT, NT};
+        bool waited = false;  // constant-folded: the solve is fully unrolled
+        mbar_wait(&bar[0], 0);
+        solve_block_b<Q>(
+            [&](int k) {
+                if (k >= Dm::C_Y && !waited) {
+                    mbar_wait(&bar[1], 0);
+                    waited = true;
+                }
+                return col[k * NT];
+            },
+            eps_add, eps_mul, StagedModel{col + Dm::C_S * NT}, B);
+    }
+    __syncthreads();
+    // coalesced store of the nb staged models: [bx0 + b][i], i < MS (pad floats = 0)
+    float* dst = models + ((size_t)(f * By + by) * Bx + bx0) * MS;
+    for (int L = t; L < nb * MS; L += NT) {
+        const int b = L / MS, i = L - b * MS;
+        dst[L] = i < 3 * (Q + 1) ? StagedModel{sms + Dm::C_S * NT + b}[i] : 0.0f;
+    }
 }
 
 // ===========================================================================

@@ -32,10 +32,10 @@ int main(int argc, char** argv)
         make_tmap_planes(&a.fit.ty, Y, W, H, nf * 3, kSeg, 3);
         make_tmap_planes(&a.app.tg, G, W, H, nf * Q, kSeg, Q);
         make_tmap_3d(&a.tmom, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, nf * Dims<Q>::KM, halo_x(R),
-                     kTileTY + 2 * R, tile_g(R));
+                     kTileTY + 2 * R, kFusedG);
         a.fit.mom = mom, a.fit.W = W, a.fit.H = H, a.fit.Bx = Bx, a.fit.Bxp = Bxp, a.fit.By = By, a.fit.nseg = W / kSeg;
         a.app.models = M, a.app.out = O, a.app.W = W, a.app.H = H, a.app.D = D, a.app.Bx = Bx, a.app.By = By;
-        a.app.nseg = W / kSeg, a.app.nband = apply_nband(H, D, By);
+        a.app.nseg = W / kSeg, a.app.nband = apply_nband(H, D, By), a.app.nsub = 1;
         a.taps.R = R;
         for (int i = -R; i <= R; ++i) a.taps.g[R + i] = 1.0;
         a.nrt = (By + 3) / 4, a.ncx = (Bx + 31) / 32, a.fit_done = flags, a.solve_done = flags + nf * By, a.n = nf;

@@ -98,7 +98,7 @@ int main()
     ApplyArgs aa;
     make_tmap_planes(&aa.tg, G, W, H, NF * Q, kSeg, Q);
     aa.models = M, aa.out = O, aa.W = W, aa.H = H, aa.D = D, aa.Bx = Bx, aa.By = By;
-    aa.nseg = (W + kSeg - 1) / kSeg, aa.nband = apply_nband(H, D, By);
+    aa.nseg = (W + kSeg - 1) / kSeg, aa.nband = apply_nband(H, D, By), aa.nsub = 1;
     using AC = ApplyCfg<Q>;
     cudaFuncSetAttribute(k_apply_stream<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AC::SMEM);
     for (int nf : {1, 4}) {
