@@ -349,7 +349,7 @@ def run_flr(args, cfg, rank, world, local_rank):
         call(i)
     torch.cuda.synchronize()
 
-    # ---- CUDA graphs: one for a full pool rotation (traced), one for the remainder
+    # ---- CUDA graphs: a full pool rotation and the remainder (timed), a traced rotation
     K = args.steps
     use_graph = not args.no_graph
     graphs = {}
@@ -361,18 +361,22 @@ def run_flr(args, cfg, rank, world, local_rank):
                 call(i)
         torch.cuda.synchronize()
 
-        def capture(nsteps):
+        def capture(nsteps, traced):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=side):
                 for i in range(nsteps):
-                    call(i, trace=traces[i])
+                    call(i, trace=traces[i] if traced else None)
             return g
 
+        # the timed graphs carry no events between kernels (an event node would serialise
+        # the programmatic-dependent launches); per-kernel durations come from a traced
+        # replay of the same steps right after the timed region
         reps, rem = divmod(K, pool)
         if reps:
-            graphs["full"] = capture(pool)
+            graphs["full"] = capture(pool, False)
         if rem:
-            graphs["rem"] = capture(rem)
+            graphs["rem"] = capture(rem, False)
+        graphs["traced"] = capture(pool, True)
         torch.cuda.synchronize()
 
     t_start = torch.cuda.Event(enable_timing=True)
@@ -392,22 +396,30 @@ def run_flr(args, cfg, rank, world, local_rank):
                 graphs["rem"].replay()
         else:
             for i in range(K):
-                call(i, trace=traces[i % pool])
+                call(i)
         t_stop.record(stream)
         torch.cuda.synchronize()
+        # traced pass (not part of the value): events between the kernels of each step
+        per_kernel_acc = {n: [] for n in kernel_names}
+        for _ in range(max(1, min(K, 400) // pool)):
+            if use_graph:
+                graphs["traced"].replay()
+            else:
+                for i in range(pool):
+                    call(i, trace=traces[i])
+            torch.cuda.synchronize()
+            for tr in traces:
+                evs = tr._keep[1]
+                for j in range(min(len(kernel_names), tr.recorded - 1 if tr.recorded else len(evs) - 1)):
+                    per_kernel_acc[kernel_names[j]].append(evs[j].elapsed_time(evs[j + 1]))
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_stop)
     clocks = sampler.summary()
 
-    # per-launch durations from the last recorded pool rotation
+    # per-launch durations from the traced pass (launch gaps included)
     names = kernel_names
-    per_kernel = {n: [] for n in names}
-    used = traces if (not use_graph or K >= pool) else traces[:K]
-    for tr in used:
-        evs = tr._keep[1]
-        for j in range(min(len(names), tr.recorded - 1 if tr.recorded else len(evs) - 1)):
-            per_kernel[names[j]].append(evs[j].elapsed_time(evs[j + 1]))
+    per_kernel = per_kernel_acc
     avg_ms = {n: (sum(v) / len(v) if v else None) for n, v in per_kernel.items()}
 
     ms_max = fd.max_over_ranks(ms, device=dev)

@@ -72,8 +72,8 @@ template <int Q, int D>
 static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
                       cudaStream_t s)
 {
-    static const bool use_tma = std::getenv("FLR_FIT_TMA") != nullptr;
-    if (!use_tma && vec_ok(G, W) && vec_ok(Y, W)) {  // default: LDG-prefetch persistent kernel
+    static const bool use_ldg = std::getenv("FLR_FIT_LDG") != nullptr;
+    if (use_ldg && vec_ok(G, W) && vec_ok(Y, W)) {  // LDG-prefetch persistent kernel (memory-latency bound)
         FitLdgArgs la{G, Y, mom, W, H, Bx, mom_pitch(Bx), By, cdiv(W, kSeg)};
         const int items = n * By * la.nseg;
         const int grid = min(num_sms(), cdiv(items, kFitLdgWarps));
@@ -112,7 +112,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     const cudaStream_t s = ctx.s;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
-        ctx.before(!vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_TMA") ? "k_fit_stream" : "k_fit_ldg");
+        ctx.before(!vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : "k_fit_stream");
         if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s);
         else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s);
         else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s);

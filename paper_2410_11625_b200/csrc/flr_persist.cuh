@@ -31,10 +31,10 @@ struct RingCfg {
     static constexpr int THREADS = NSW * 32;
 };
 #ifndef FLR_FIT_S
-#define FLR_FIT_S 3
+#define FLR_FIT_S 4
 #endif
 #ifndef FLR_FIT_MAXW
-#define FLR_FIT_MAXW 10
+#define FLR_FIT_MAXW 8
 #endif
 template <int Q>
 using FitCfg = RingCfg<StreamDims<Q>::STG_FIT, 0, FLR_FIT_S, FLR_FIT_MAXW>;
