@@ -3,6 +3,7 @@
 // caller's stream.  No allocation, no synchronisation, no host<->device copies.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/flr.h"
@@ -60,7 +61,7 @@ Layout layout(int n, int Q, int Bx, int By)
     off += align256(nbp * km_of(Q) * sizeof(double));
     L.models = off;
     off += align256(nb * mstride_of(Q) * sizeof(float));
-    L.flags = off;  // fused schedule: fit_done [n][By] + solve_done [n][ceil(By/4)]
+    L.flags = off;  // row counters: fit_done [n][By] + K2/solve_done [n][ceil(By/4)] (wavefronts)
     off += align256(sizeof(int) * (size_t)n * (By + (By + 3) / 4));
     L.total = off;
     return L;
@@ -148,6 +149,10 @@ flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, co
     char* base = (char*)ws;
     const double sblk = p->sigma / ((double)D * p->upsample);
     const Taps taps = make_taps(sblk, effective_radius(p));
+    // opt-in row wavefront across the three grids (FLR_WAVE=1): measured slower on one
+    // B200 (the per-item release and the per-call flag reset cost more than the overlap)
+    static const bool wave = std::getenv("FLR_WAVE") != nullptr;
+    ctx.wave_flags = wave ? (int*)(base + L.flags) : nullptr;
     FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, G, Y, (float*)(base + L.raw),
                                       (double*)(base + L.mom), (double*)(base + L.hb), models,
                                       mstride, p->eps_add, p->eps_mul, taps, ctx)));

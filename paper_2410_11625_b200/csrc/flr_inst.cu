@@ -68,9 +68,10 @@ static int num_sms()
     return sms;
 }
 
+// returns true when the TMA-ring kernel ran with `done` row counters (K2 may then wait per row)
 template <int Q, int D>
-static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
-                      cudaStream_t s)
+static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
+                      int* done, cudaStream_t s)
 {
     static const bool use_ldg = std::getenv("FLR_FIT_LDG") != nullptr;
     if (use_ldg && vec_ok(G, W) && vec_ok(Y, W)) {  // LDG-prefetch persistent kernel (memory-latency bound)
@@ -78,19 +79,20 @@ static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
         const int items = n * By * la.nseg;
         const int grid = min(num_sms(), cdiv(items, kFitLdgWarps));
         launch_pdl(k_fit_ldg<Q, D>, dim3(grid), dim3(kFitLdgWarps * 32), 0, s, la, n);
-        return;
+        return false;
     }
     FitArgs a;
     if (vec_ok(G, W) && vec_ok(Y, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q) &&
         make_tmap_planes(&a.ty, Y, W, H, n * 3, kSeg, 3)) {  // TMA-fed persistent path
         a.mom = mom;
         a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
+        a.done = done;
         using C = FitCfg<Q>;
         const int items = n * By * a.nseg;
         const int grid = min(num_sms(), cdiv(items, C::NSW));
         set_smem(k_fit_stream<Q, D>, C::SMEM);
         launch_pdl(k_fit_stream<Q, D>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
-        return;
+        return done != nullptr;
     }
     const size_t sm = fit_smem_bytes<Q, D>();
     dim3 grid(cdiv(W, 128), By, n), block(FitGeom<D>::THREADS);
@@ -102,6 +104,7 @@ static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
         set_smem(k_fit_moments<Q, D, false>, sm);
         k_fit_moments<Q, D, false><<<grid, block, sm, s>>>(W, H, Bx, Bxp, By, G, Y, mom);
     }
+    return false;
 }
 
 template <int Q>
@@ -110,12 +113,18 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
                 double em, const Taps& taps, LaunchCtx& ctx)
 {
     const cudaStream_t s = ctx.s;
+    // wavefront flags: fit_done [n][By] | k2_done [n][ceil(By / kK2TY)]
+    int* fit_done = ctx.wave_flags;
+    int* k2_done = fit_done ? fit_done + (size_t)n * By : nullptr;
+    if (fit_done) cudaMemsetAsync(fit_done, 0, sizeof(int) * (size_t)n * (By + cdiv(By, kK2TY)), s);
+    ctx.wave_k2 = nullptr;
+    bool fit_signals = false;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
         ctx.before(!vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : "k_fit_stream");
-        if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s);
-        else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s);
-        else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s);
+        if (D == 4) fit_signals = launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, fit_done, s);
+        else if (D == 8) fit_signals = launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, fit_done, s);
+        else fit_signals = launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, fit_done, s);
     } else {
         ctx.before("k_moments_small");
         k_moments_small<Q><<<dim3(cdiv(Bx, 128), By, n), 128, 0, s>>>(W, H, Bx, By, D, G, Y, raw);
@@ -147,7 +156,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
         ctx.before("k_blur_solve_tile");                                                                    \
         set_smem(k_blur_solve_tile<Q, RR>, KG::SMEM);                                                       \
         launch_pdl(k_blur_solve_tile<Q, RR>, grid, dim3(kK2Threads), KG::SMEM, s, tm, Bx, By, models, ea, em, \
-                   taps);                                                                                   \
+                   taps, (const int*)(fit_signals ? fit_done : nullptr), cdiv(W, kSeg), k2_done);           \
         k2tile = true;                                                                                      \
         break;                                                                                              \
     }
@@ -155,6 +164,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
 #undef FLR_KT
     }
     if (k2tile) {
+        if (k2_done) ctx.wave_k2 = k2_done, ctx.wave_nrt = cdiv(By, kK2TY), ctx.wave_target = cdiv(Bx, kK2TX);
     } else if (!tile && R >= 1 && R <= kTileMaxR && blur_rows_smem(Bx, R) <= 227 * 1024 &&
         (size_t)n * Dims<Q>::KM <= 65535) {
         ctx.before("k_blur_rows");
@@ -221,6 +231,8 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
                 a.nsub *= 2;
             if (const char* e = std::getenv("FLR_APPLY_NSUB")) a.nsub = std::max(1, std::atoi(e));
             if (D % a.nsub) a.nsub = 1;
+            a.ready = ctx.wave_k2, a.ready_target = ctx.wave_target, a.nrt = ctx.wave_nrt;
+            ctx.wave_k2 = nullptr;
             const int items = n * a.nseg * a.nband * a.nsub;
             const int grid = min(num_sms(), cdiv(items, C::NSW));
             ctx.before("k_apply_stream");

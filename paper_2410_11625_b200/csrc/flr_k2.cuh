@@ -56,7 +56,8 @@ struct K2Geom {
 template <int Q, int R>
 __global__ void __launch_bounds__(kK2Threads, 1)
     k_blur_solve_tile(const __grid_constant__ CUtensorMap tm, int Bx, int By, float* __restrict__ models,
-                      double eps_add, double eps_mul, const __grid_constant__ Taps t)
+                      double eps_add, double eps_mul, const __grid_constant__ Taps t, const int* wait_rows,
+                      int wait_target, int* signal)
 {
     using Dm = Dims<Q>;
     using KG = K2Geom<Q, R>;
@@ -80,7 +81,15 @@ __global__ void __launch_bounds__(kK2Threads, 1)
         fence_mbar_init();
     }
     pdl_trigger();
-    pdl_wait();  // the moment field comes from the previous grid
+    if (!wait_rows) {
+        pdl_wait();  // the moment field comes from the previous grid
+    } else {  // wavefront: only the FIT rows this tile reads (+- R), one polling thread per row
+        const int rr = by0 - R + tid;
+        if (tid < TY + 2 * R && rr >= 0 && rr < By)
+            while (ld_acquire(&wait_rows[f * By + rr]) < wait_target) __nanosleep(64);
+        __syncthreads();
+        if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+    }
     __syncthreads();
     if (tid == 0)
         for (int g = 0; g < S && g < NG; ++g) issue(g);
@@ -179,6 +188,10 @@ __global__ void __launch_bounds__(kK2Threads, 1)
         float* dst = models + ((size_t)(f * By + by0 + r) * Bx + bx0) * MS;
         const float* src = mstage + r * TX * MS;
         for (int i = tid; i < nbx * MS; i += kK2Threads) dst[i] = src[i];
+    }
+    if (signal) {  // publish this tile's models to the APPLY wavefront
+        __syncthreads();
+        if (tid == 0) red_release_add(&signal[f * gridDim.y + blockIdx.y], 1);
     }
 }
 

@@ -57,6 +57,12 @@ struct LaunchCtx {
     int recorded = 0;
     bool capturing = false;   // stream capture: events become graph event-record nodes
     bool unsupported = false; // set by launchers compiled out of a dev build (FLR_STUB)
+    // row wavefront across the K1 -> K2 -> K3 grids (flags zeroed per call): K2 tiles wait
+    // on per-row FIT counters, APPLY items on per-tile-row K2 counters, instead of on the
+    // completion of the whole previous grid (griddepcontrol.wait)
+    int* wave_flags = nullptr;     // workspace flag area, nullptr = off
+    const int* wave_k2 = nullptr;  // set by launch_fit when K2 signals: [n][wave_nrt]
+    int wave_nrt = 0, wave_target = 0;
     void record()
     {
         if (events && recorded < capacity) {

@@ -113,6 +113,13 @@ struct ApplySeq {
     {
         if (it >= nitems) return false;
         if (row < 0) {
+            if (a->ready) {  // wavefront: the K2 tile rows (8 block rows each) holding rows j0, j1
+                const int m0 = g.j0 / 8, m1 = g.j1 / 8;
+                const int v0 = ld_relaxed(&a->ready[f * a->nrt + m0]), v1 = ld_relaxed(&a->ready[f * a->nrt + m1]);
+                if (v0 < a->ready_target || v1 < a->ready_target) return false;  // retried from ring_wait
+                fence_acquire();
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk copy
+            }
             apply_issue_models<Q>(*a, g, f, dst, bar, pm);
             row = g.y0;
         } else {
@@ -154,6 +161,10 @@ __global__ void __launch_bounds__(FitCfg<Q>::THREADS, 1) k_fit_stream(const __gr
     for (int it = first; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it % per_frame;
         fit_consume<Q, D>(r, seq, a, f, rem / a.nseg, rem % a.nseg, lane);
+        if (a.done) {  // publish the item's moments to the K2 wavefront (release is cumulative
+            __syncwarp();  // over the lanes' stores ordered before it by the warp barrier)
+            if (lane == 0) red_release_add(&a.done[f * a.By + rem / a.nseg], 1);
+        }
 #ifdef FLR_DBG_TIMES
         ++nit;
 #endif
@@ -205,7 +216,7 @@ __global__ void __launch_bounds__(ApplyCfg<Q>::THREADS, 1) k_apply_stream(const 
     seq.pg = policy_evict_first(), seq.pm = policy_evict_normal();  // last use of the guides
     seq.decode();
     pdl_trigger();
-    pdl_wait();  // models come from the previous grid
+    if (!a.ready) pdl_wait();  // models come from the previous grid (or per tile row, see ApplySeq)
     if (lane == 0) ring_fill(r, seq);
     for (int it = first; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it % per_frame;

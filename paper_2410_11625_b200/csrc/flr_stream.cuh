@@ -104,6 +104,7 @@ struct FitArgs {
     CUtensorMap ty;  // radiance [n*3][H][W], box {128, 1, 3}
     double* mom;     // [n][KM][By][Bxp]
     int W, H, Bx, Bxp, By, nseg;
+    int* done;       // optional [n][By] row counters (+1 per finished item, release)
 };
 
 template <int Q, int D>
@@ -395,6 +396,8 @@ struct ApplyArgs {
     float* out;           // [n][3][H][W]
     int W, H, D, Bx, By, nseg, nband;
     int nsub;  // sub-bands per band (D % nsub == 0): more, smaller APPLY items for one frame
+    const int* ready;  // optional [n][nrt] K2 tile-row counters (complete at ready_target)
+    int ready_target, nrt;
 };
 
 __host__ __device__ inline int apply_nband(int H, int D, int By)
