@@ -1,0 +1,231 @@
+// flr_fitws.cuh -- K1 (block moments) as a warp-specialised TMA pipeline.
+//
+// One CTA per SM: kFitWsNC consumer warps + 1 producer warp.  Lane c of the producer
+// walks consumer c's item sequence and keeps its kFitWsS-stage shared-memory ring full
+// (one TMA pair per pixel row: the Q guide planes and the 3 radiance planes of 128
+// pixels); consumers wait on the stage's `full` mbarrier, accumulate, and arrive on its
+// `empty` mbarrier.  Consumer warps therefore run no producer code at all: per row they
+// do 22 shared loads, 8 + 71 packed fp32x2 operations per pixel pair and two barrier ops.
+//
+// Accumulation is in PIXEL pairs (fma.rn.f32x2 of two pixels' products, both operands
+// vectors): a lane's 4 pixels are 2 pairs of the same block, so every packed operand
+// comes straight from an 8-byte shared load with no repacking, and the pair halves are
+// added once per item.  Sums are taken about the block's top-left pixel c (design rule
+// H1) and un-shifted to fp64 in the epilogue (FitAcc::store's algebra).
+#pragma once
+#include "flr_stream.cuh"
+
+namespace flr {
+
+constexpr int kFitWsNC = 7;  // consumer warps (+1 producer = 8 warps: 2 per SMSP keeps the 255-register cap)
+constexpr int kFitWsS = 4;   // ring stages per consumer
+
+template <int Q>
+struct FitWsCfg {
+    static constexpr int NC = kFitWsNC, S = kFitWsS, THREADS = (NC + 1) * 32;
+    static constexpr int STG = StreamDims<Q>::STG_FIT;  // floats per stage (one pixel row)
+    static constexpr size_t BAR_OFF = (size_t)NC * S * STG * sizeof(float);
+    static constexpr size_t SMEM = BAR_OFF + 2 * NC * S * sizeof(uint64_t);
+};
+
+// per-lane accumulators of one item, pixel-pair packed
+template <int Q>
+struct FitAccPix {
+    using Dm = Dims<Q>;
+    f2 U[Q], S[Dm::NS], Y[3], XY[3 * Q];
+    __device__ __forceinline__ void zero()
+    {
+#pragma unroll
+        for (int j = 0; j < Q; ++j) U[j] = 0ull;
+#pragma unroll
+        for (int s = 0; s < Dm::NS; ++s) S[s] = 0ull;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Y[c] = 0ull;
+#pragma unroll
+        for (int k = 0; k < 3 * Q; ++k) XY[k] = 0ull;
+    }
+    // d[j]: shifted guide j of the pixel pair, y[c]: radiance
+    __device__ __forceinline__ void add(const f2 (&d)[Q], const f2 (&y)[3])
+    {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Y[c] = add2(Y[c], y[c]);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) U[j] = add2(U[j], d[j]);
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+            for (int j = i; j < Q; ++j) S[Dm::s_idx(i, j) - Dm::C_S] = fma2(d[i], d[j], S[Dm::s_idx(i, j) - Dm::C_S]);
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) XY[j * 3 + c] = fma2(d[j], y[c], XY[j * 3 + c]);
+    }
+};
+
+// fold the pair halves and the m lanes of a block (xor shuffles) into plain fp32 sums
+template <int N>
+__device__ __forceinline__ void fold_pairs(const f2 (&in)[N], float (&out)[N], int m_lanes)
+{
+#pragma unroll
+    for (int k = 0; k < N; ++k) out[k] = lo2(in[k]) + hi2(in[k]);
+    for (int m = 1; m < m_lanes; m <<= 1)
+#pragma unroll
+        for (int k = 0; k < N; ++k) out[k] += __shfl_xor_sync(0xffffffffu, out[k], m);
+}
+
+// the rows of one item for one consumer warp (k: rows consumed so far by this warp)
+template <int Q, int D, bool EDGE>
+__device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], const float* ring, uint64_t* full,
+                                            uint64_t* empty, int& k, int rows, int lane, int lb0, int x0, int W)
+{
+    constexpr int S = kFitWsS, STG = FitWsCfg<Q>::STG;
+    {  // the block shift c = its top-left pixel (first row of the item)
+        mbar_wait(&full[k % S], (k / S) & 1);
+        const float* st = ring + (k % S) * STG;
+#pragma unroll
+        for (int j = 0; j < Q; ++j) cs[j] = st[j * kSeg + lb0];
+    }
+#pragma unroll 1  // keep the row body resident in the instruction cache
+    for (int rr = 0; rr < rows; ++rr, ++k) {
+        const int slot = k % S;
+        mbar_wait(&full[slot], (k / S) & 1);
+        const float* st = ring + slot * STG;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            f2 d[Q], y[3];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) d[j] = reinterpret_cast<const f2*>(st + j * kSeg)[2 * lane + h];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) y[c] = reinterpret_cast<const f2*>(st + (Q + c) * kSeg)[2 * lane + h];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) d[j] = sub2(d[j], bc2(cs[j]));
+            if (EDGE) {  // pixels past the image arrive as zeros: make them contribute nothing
+                const bool in0 = x0 + 2 * h < W, in1 = x0 + 2 * h + 1 < W;
+#pragma unroll
+                for (int j = 0; j < Q; ++j) d[j] = pk2(in0 ? lo2(d[j]) : 0.f, in1 ? hi2(d[j]) : 0.f);
+            }
+            acc.add(d, y);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);  // values are in registers: free the stage
+    }
+}
+
+template <int Q, int D>
+__global__ void __launch_bounds__(FitWsCfg<Q>::THREADS, 1) k_fit_ws(const __grid_constant__ FitArgs a, int n)
+{
+    using C = FitWsCfg<Q>;
+    using Dm = Dims<Q>;
+    constexpr int NC = C::NC, S = C::S, STG = C::STG, DQ = D / 4;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float* stages = reinterpret_cast<float*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF);
+    uint64_t* empty = full + NC * S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NC * S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int per_frame = a.By * a.nseg, nitems = n * per_frame, GW = gridDim.x * NC;
+    pdl_trigger();
+    pdl_wait();  // caller data may come from the previous grid
+
+    if (warp == NC) {
+        // ---------------- producer: lane c feeds consumer c ----------------
+        if (lane >= NC) return;
+        const int c = lane;
+        const uint64_t pg = std_policy_guides_fit(), py = policy_evict_first();
+        int it = blockIdx.x * NC + c, row = 0, rows = 0, f = 0, by = 0, sg = 0;
+        auto decode = [&]() {
+            if (it >= nitems) return;
+            f = it / per_frame;
+            const int rem = it - f * per_frame;
+            by = rem / a.nseg;
+            sg = rem - by * a.nseg;
+            rows = min(D, a.H - by * D);
+        };
+        decode();
+        // the NC lanes stay converged: each round, every lane whose next slot is free
+        // (non-blocking test) issues one row for its consumer
+        int k = 0;
+        constexpr unsigned mask = (1u << NC) - 1;
+        while (__any_sync(mask, it < nitems)) {
+            const int slot = k % S;
+            if (it < nitems && (k < S || mbar_test_wait(&empty[c * S + slot], ((k / S) - 1) & 1))) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                fit_issue_row<Q, D>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
+                                    pg, py);
+                ++k;
+                if (++row == rows) {
+                    row = 0;
+                    it += GW;
+                    decode();
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warp ----------------
+    const int w = warp;
+    float* ring = stages + (size_t)w * S * STG;
+    int k = 0;  // rows consumed
+    for (int it = blockIdx.x * NC + w; it < nitems; it += GW) {
+        const int f = it / per_frame, rem = it - f * per_frame, by = rem / a.nseg, sg = rem - by * a.nseg;
+        const int rows = min(D, a.H - by * D);
+        const int x0 = sg * kSeg + lane * 4, bx = x0 / D, lb0 = (lane / DQ) * D;
+        float cs[Q];
+        FitAccPix<Q> acc;
+        acc.zero();
+        if (sg * kSeg + kSeg > a.W)  // segment reaches past the image
+            fit_ws_rows<Q, D, true>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W);
+        else
+            fit_ws_rows<Q, D, false>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W);
+        // epilogue: fold, then un-shift to fp64 and store (lanes of a block split the components)
+        float u[Q], sv[Dm::NS], yc[3], xy[3 * Q];
+        fold_pairs(acc.U, u, DQ);
+        fold_pairs(acc.S, sv, DQ);
+        fold_pairs(acc.Y, yc, DQ);
+        fold_pairs(acc.XY, xy, DQ);
+        if (bx < a.Bx) {
+        const int gi = lane % DQ;
+        const double nn = (double)(min(D, a.W - bx * D) * rows);
+        const size_t cst = (size_t)a.By * a.Bxp;
+        double* out = a.mom + (size_t)f * Dm::KM * cst + (size_t)by * a.Bxp + bx;
+        auto put = [&](int kk, double v) {
+            if (kk % DQ == gi) out[(size_t)kk * cst] = v;
+        };
+        put(Dm::C_N, nn);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) put(Dm::C_U + j, fma(nn, (double)cs[j], (double)u[j]));
+        // S_ij = S'_ij + c_i u'_j + c_j u'_i + n c_i c_j
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+            for (int j = i; j < Q; ++j) {
+                double v = (double)sv[Dm::s_idx(i, j) - Dm::C_S];
+                v = fma((double)cs[i], (double)u[j], v);
+                v = fma((double)cs[j], (double)u[i], v);
+                v = fma(nn * (double)cs[i], (double)cs[j], v);
+                put(Dm::s_idx(i, j), v);
+            }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) put(Dm::C_Y + c, (double)yc[c]);
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                put(Dm::C_XY + j * 3 + c, fma((double)cs[j], (double)yc[c], (double)xy[j * 3 + c]));
+        }
+        if (a.done) {
+            __syncwarp();
+            if (lane == 0) red_release_add(&a.done[f * a.By + by], 1);
+        }
+    }
+}
+
+}  // namespace flr

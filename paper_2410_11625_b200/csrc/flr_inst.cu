@@ -7,6 +7,7 @@
 #include "flr_tiles.cuh"
 #include "flr_persist.cuh"
 #include "flr_k2.cuh"
+#include "flr_fitws.cuh"
 #if FLR_Q == 4 || FLR_Q == 8
 #include "flr_fused.cuh"
 #endif
@@ -87,11 +88,19 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
         a.mom = mom;
         a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
         a.done = done;
-        using C = FitCfg<Q>;
         const int items = n * By * a.nseg;
-        const int grid = min(num_sms(), cdiv(items, C::NSW));
-        set_smem(k_fit_stream<Q, D>, C::SMEM);
-        launch_pdl(k_fit_stream<Q, D>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+        static const bool ring = std::getenv("FLR_FIT_RING") != nullptr;
+        if (ring) {  // per-warp self-feeding rings (lane 0 of each warp issues its own TMA)
+            using C = FitCfg<Q>;
+            const int grid = min(num_sms(), cdiv(items, C::NSW));
+            set_smem(k_fit_stream<Q, D>, C::SMEM);
+            launch_pdl(k_fit_stream<Q, D>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+        } else {  // default: warp-specialised (one producer warp feeds 7 consumer warps)
+            using C = FitWsCfg<Q>;
+            const int grid = min(num_sms(), cdiv(items, C::NC));
+            set_smem(k_fit_ws<Q, D>, C::SMEM);
+            launch_pdl(k_fit_ws<Q, D>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+        }
         return done != nullptr;
     }
     const size_t sm = fit_smem_bytes<Q, D>();
@@ -121,7 +130,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     bool fit_signals = false;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
-        ctx.before(!vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : "k_fit_stream");
+        ctx.before(!vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : std::getenv("FLR_FIT_RING") ? "k_fit_stream" : "k_fit_ws");
         if (D == 4) fit_signals = launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, fit_done, s);
         else if (D == 8) fit_signals = launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, fit_done, s);
         else fit_signals = launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, fit_done, s);

@@ -9,13 +9,16 @@
 
 namespace flr {
 
-// L2 policy of the fit pass's guide reads (FLR_FIT_GUIDES_EVICT_LAST builds keep them resident)
+// L2 policy of the fit pass's guide reads.  A 1080p frame's guides (66 MB) do not survive
+// in L2 until the apply pass anyway (measured: apply re-reads them all from DRAM), so by
+// default they are streamed (evict_first) and the L2 keeps the moment field for K2;
+// FLR_FIT_GUIDES_LAST builds try to keep them resident instead.
 __device__ __forceinline__ uint64_t std_policy_guides_fit()
 {
-#ifdef FLR_FIT_GUIDES_NORMAL
-    return policy_evict_normal();
-#else
+#ifdef FLR_FIT_GUIDES_LAST
     return policy_evict_last();
+#else
+    return policy_evict_first();
 #endif
 }
 
@@ -148,7 +151,6 @@ __global__ void __launch_bounds__(FitCfg<Q>::THREADS, 1) k_fit_stream(const __gr
     Ring r = sm.ring(w);
     FitSeq<Q, D> seq;
     seq.a = &a, seq.it = first, seq.nitems = nitems, seq.per_frame = per_frame, seq.step = GW;
-    // guides are read again by the apply pass: keep them in L2; radiance is read once
     seq.pg = std_policy_guides_fit(), seq.py = policy_evict_first();
     seq.decode();
     pdl_trigger();
