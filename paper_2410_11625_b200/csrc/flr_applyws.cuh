@@ -1,0 +1,211 @@
+// flr_applyws.cuh -- K3 (apply the blended per-block models, R4) as a
+// warp-specialised TMA pipeline, like flr_fitws.cuh.
+//
+// One CTA per SM: kApplyWsNC consumer warps + 1 producer warp.  Lane c of the producer
+// walks consumer c's APPLY items (sub-band of D/nsub output rows x 128 pixels) and keeps
+// two rings full: the item's 2 x 18 staged models (two 1-D bulk copies, 2 stages) and its
+// guide rows (one 3-D TMA box {128, 1, Q} per row, kApplyWsS stages).  Consumers run no
+// producer code: per item each lane keeps its two model columns (top row and bottom-top
+// difference) in registers; per row it forms A_y = top + t_y (bottom - top), reads its
+// pixel quad of the Q guide planes, and applies I = (1 - t_x) x~.A_y(i0) + t_x x~.A_y(i1)
+// with packed fp32x2 FMAs, streaming the 3 output planes out (st.global.cs).
+#pragma once
+#include "flr_stream.cuh"
+
+namespace flr {
+
+constexpr int kApplyWsNC = 7;  // consumer warps (+1 producer = 8 warps, 255-register cap)
+constexpr int kApplyWsS = 4;   // guide-row stages per consumer
+constexpr int kApplyWsM = 2;   // model stages per consumer
+
+template <int Q>
+struct ApplyWsCfg {
+    using SD = StreamDims<Q>;
+    static constexpr int NC = kApplyWsNC, S = kApplyWsS, SM = kApplyWsM, THREADS = (NC + 1) * 32;
+    static constexpr int ROWF = Q * kSeg;                 // floats per guide-row stage
+    static constexpr int MODF = 2 * kApplyNCol * SD::MS;  // floats per model stage
+    static constexpr int WARPF = (S * ROWF + SM * MODF + 31) / 32 * 32;  // 128-byte aligned regions
+    static constexpr size_t BAR_OFF = (size_t)NC * WARPF * sizeof(float);
+    static constexpr int NBAR = 2 * (S + SM);  // full + empty per stage
+    static constexpr size_t SMEM = BAR_OFF + (size_t)NC * NBAR * sizeof(uint64_t);
+    static_assert(WARPF % 32 == 0 && ROWF % 32 == 0 && MODF % 4 == 0, "16-byte aligned stages");
+    static_assert(SMEM <= 232448, "apply pipeline exceeds 227 KB of shared memory");
+};
+
+template <int Q>
+__global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __grid_constant__ ApplyArgs a, int n)
+{
+    using C = ApplyWsCfg<Q>;
+    using SD = StreamDims<Q>;
+    constexpr int NC = C::NC, S = C::S, SM = C::SM, MS = SD::MS;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NC * C::NBAR; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int per_frame = a.nband * a.nsub * a.nseg, nitems = n * per_frame, GW = gridDim.x * NC;
+    pdl_trigger();
+    pdl_wait();  // the models come from the previous grid
+
+    auto geom = [&](int it, int& f) {
+        f = it / per_frame;
+        const int rem = it - f * per_frame;
+        return apply_geom(a, rem / a.nseg, rem - (rem / a.nseg) * a.nseg);
+    };
+
+    if (warp == NC) {
+        // ---------------- producer: lane c feeds consumer c ----------------
+        if (lane >= NC) return;
+        const int c = lane;
+        float* base = reinterpret_cast<float*>(smem_raw) + (size_t)c * C::WARPF;
+        float* rows_st = base;
+        float* mod_st = base + S * C::ROWF;
+        uint64_t* rfull = bars + c * C::NBAR;
+        uint64_t* rempty = rfull + S;
+        uint64_t* mfull = rempty + S;
+        uint64_t* mempty = mfull + SM;
+        const uint64_t pg = policy_evict_first(), pm = policy_evict_normal();
+        int it = blockIdx.x * NC + c, f = 0, y = 0, kr = 0, km = 0;
+        ApplyGeom g;
+        bool need_models = true;
+        auto next_item = [&]() {  // skip empty sub-bands (rows outside the image)
+            for (; it < nitems; it += GW) {
+                g = geom(it, f);
+                if (g.y0 < g.y1) break;
+            }
+            y = g.y0;
+            need_models = true;
+        };
+        next_item();
+        constexpr unsigned mask = (1u << NC) - 1;
+        while (__any_sync(mask, it < nitems)) {
+            if (it >= nitems) continue;
+            if (need_models) {
+                const int s = km % SM;
+                if (km < SM || mbar_test_wait(&mempty[s], ((km / SM) - 1) & 1)) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    apply_issue_models<Q>(a, g, f, mod_st + s * C::MODF, &mfull[s], pm);
+                    ++km;
+                    need_models = false;
+                }
+            } else {
+                const int s = kr % S;
+                if (kr < S || mbar_test_wait(&rempty[s], ((kr / S) - 1) & 1)) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    apply_issue_row<Q>(a, g, f, y, rows_st + s * C::ROWF, &rfull[s], pg);
+                    ++kr;
+                    if (++y == g.y1) {
+                        it += GW;
+                        next_item();
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warp ----------------
+    const int w = warp;
+    float* base = reinterpret_cast<float*>(smem_raw) + (size_t)w * C::WARPF;
+    const float* rows_st = base;
+    const float* mod_st = base + S * C::ROWF;
+    uint64_t* rfull = bars + w * C::NBAR;
+    uint64_t* rempty = rfull + S;
+    uint64_t* mfull = rempty + S;
+    uint64_t* mempty = mfull + SM;
+    const float invD = 1.0f / (float)a.D;
+    const size_t plane = (size_t)a.W * a.H;
+    constexpr int MP = MS / 2;  // model float pairs
+    int kr = 0, km = 0;
+    for (int it = blockIdx.x * NC + w; it < nitems; it += GW) {
+        int f;
+        const ApplyGeom g = geom(it, f);
+        if (g.y0 >= g.y1) continue;
+        const int xq = g.xs + lane * 4;  // the lane's quad
+        const bool active = xq < a.W;
+        const float fxq = ((float)xq + 0.5f) * invD - 0.5f;
+        const int ib = (int)floorf(fxq);
+        const int c0 = min(max(ib, 0), a.Bx - 1) - g.ic0;
+        const int c1 = min(max(ib + 1, 0), a.Bx - 1) - g.ic0;
+        f2 t2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            t2[h] = pk2(((float)(xq + 2 * h) + 0.5f) * invD - 0.5f - (float)ib,
+                        ((float)(xq + 2 * h + 1) + 0.5f) * invD - 0.5f - (float)ib);
+        // the lane's two model columns, top (block row j0) and bottom (j1) -> registers:
+        // A_y = top + t_y (bottom - top) is then 2 x MS/2 packed FMAs per row
+        f2 top0[MP], dlt0[MP], top1[MP], dlt1[MP];
+        {
+            const int ms = km % SM;
+            mbar_wait(&mfull[ms], (km / SM) & 1);
+            const float* mod = mod_st + ms * C::MODF;
+#pragma unroll
+            for (int v = 0; v < MS / 4; ++v) {
+                const float4 p0 = reinterpret_cast<const float4*>(mod + c0 * MS)[v];
+                const float4 q0 = reinterpret_cast<const float4*>(mod + (kApplyNCol + c0) * MS)[v];
+                const float4 p1 = reinterpret_cast<const float4*>(mod + c1 * MS)[v];
+                const float4 q1 = reinterpret_cast<const float4*>(mod + (kApplyNCol + c1) * MS)[v];
+                top0[2 * v] = pk2(p0.x, p0.y), top0[2 * v + 1] = pk2(p0.z, p0.w);
+                top1[2 * v] = pk2(p1.x, p1.y), top1[2 * v + 1] = pk2(p1.z, p1.w);
+                dlt0[2 * v] = sub2(pk2(q0.x, q0.y), top0[2 * v]), dlt0[2 * v + 1] = sub2(pk2(q0.z, q0.w), top0[2 * v + 1]);
+                dlt1[2 * v] = sub2(pk2(q1.x, q1.y), top1[2 * v]), dlt1[2 * v + 1] = sub2(pk2(q1.z, q1.w), top1[2 * v + 1]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&mempty[ms]);  // models are in registers: free the stage
+            ++km;
+        }
+        float* O = a.out + (size_t)f * 3 * plane;
+#pragma unroll 1
+        for (int y = g.y0; y < g.y1; ++y, ++kr) {
+            const float fy = ((float)y + 0.5f) * invD - 0.5f;
+            const f2 ty2 = bc2(fy - floorf(fy));
+            const int rs = kr % S;
+            mbar_wait(&rfull[rs], (kr / S) & 1);
+            const float* st = rows_st + rs * C::ROWF;
+            float gq[Q][4];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) {
+                const float4 v = reinterpret_cast<const float4*>(st + j * kSeg)[lane];
+                gq[j][0] = v.x; gq[j][1] = v.y; gq[j][2] = v.z; gq[j][3] = v.w;
+            }
+            float m0[MS], m1[MS];
+#pragma unroll
+            for (int v = 0; v < MP; ++v) {
+                upk2(fma2(ty2, dlt0[v], top0[v]), m0[2 * v], m0[2 * v + 1]);
+                upk2(fma2(ty2, dlt1[v], top1[v]), m1[2 * v], m1[2 * v + 1]);
+            }
+            float o[3][4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // pixel pairs (2h, 2h+1)
+                f2 gp[Q];
+#pragma unroll
+                for (int j = 0; j < Q; ++j) gp[j] = pk2(gq[j][2 * h], gq[j][2 * h + 1]);
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    f2 p0 = bc2(m0[cc]), p1 = bc2(m1[cc]);
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        p0 = fma2(gp[j], bc2(m0[(1 + j) * 3 + cc]), p0);
+                        p1 = fma2(gp[j], bc2(m1[(1 + j) * 3 + cc]), p1);
+                    }
+                    upk2(fma2(t2[h], sub2(p1, p0), p0), o[cc][2 * h], o[cc][2 * h + 1]);
+                }
+            }
+            __syncwarp();  // guide stage consumed by every lane
+            if (lane == 0) mbar_arrive(&rempty[rs]);
+            if (active) {
+                float* Orow = O + (size_t)y * a.W + xq;
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc)
+                    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(Orow + cc * plane), "f"(o[cc][0]),
+                                 "f"(o[cc][1]), "f"(o[cc][2]), "f"(o[cc][3])
+                                 : "memory");
+            }
+        }
+    }
+}
+
+}  // namespace flr

@@ -8,6 +8,7 @@
 #include "flr_persist.cuh"
 #include "flr_k2.cuh"
 #include "flr_fitws.cuh"
+#include "flr_applyws.cuh"
 #if FLR_Q == 4 || FLR_Q == 8
 #include "flr_fused.cuh"
 #endif
@@ -243,10 +244,24 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
             a.ready = ctx.wave_k2, a.ready_target = ctx.wave_target, a.nrt = ctx.wave_nrt;
             ctx.wave_k2 = nullptr;
             const int items = n * a.nseg * a.nband * a.nsub;
-            const int grid = min(num_sms(), cdiv(items, C::NSW));
-            ctx.before("k_apply_stream");
-            set_smem(k_apply_stream<Q>, C::SMEM);
-            launch_pdl(k_apply_stream<Q>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+            // many items (batches): the 11-warp self-feeding rings keep more rows in flight;
+            // few items (one frame): the warp-specialised kernel's faster items win
+            // (measured 1080p: 1 frame 22.6 vs 26.6 us, 8 frames 17.8 vs 16.2 us per frame)
+            static const char* env = std::getenv("FLR_APPLY_RING");
+            const bool ring = env ? env[0] == '1' : items >= 4 * num_sms() * ApplyCfg<Q>::NSW;
+            if (ring || a.ready) {  // per-warp self-feeding rings (supports the row wavefront)
+                using C = ApplyCfg<Q>;
+                const int grid = min(num_sms(), cdiv(items, C::NSW));
+                ctx.before("k_apply_stream");
+                set_smem(k_apply_stream<Q>, C::SMEM);
+                launch_pdl(k_apply_stream<Q>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+            } else {  // default: warp-specialised (one producer warp feeds 7 consumer warps)
+                using C = ApplyWsCfg<Q>;
+                const int grid = min(num_sms(), cdiv(items, C::NC));
+                ctx.before("k_apply_ws");
+                set_smem(k_apply_ws<Q>, C::SMEM);
+                launch_pdl(k_apply_ws<Q>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+            }
             return;
         }
         dim3 grid(cdiv(cdiv(W + off, 8), kApplyUnits), cdiv(H + off, kApplyRows), n),
