@@ -95,7 +95,32 @@ KERNEL_BYTES = {
     "k_apply_tile": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
     "k_apply_px": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
     "k_flr_fused": lambda c: min_bytes_per_frame(c),
+    "k_fit_ws": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
+    "k_apply_ws": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
 }
+
+
+def k2_flops_per_frame(c):
+    """Algorithmic fp64 flops of K2 per frame: the separable blur (2 passes of 2R+1 taps on
+    each of the KM moment components) + the appendix solve (Cholesky Q^3/3, 3 right-hand
+    sides 3 Q^2, normalisation and model assembly) per block; FMA = 2 flops."""
+    Q, W, H, D = c["Q"], c["W"], c["H"], c["block"]
+    R = c.get("radius") or math.ceil(2.0 * c["sigma"] / (D * c["upsample"]) - 1e-12)
+    KM = 1 + Q + Q * (Q + 1) // 2 + 3 + 3 * Q
+    NS = Q * (Q + 1) // 2
+    blocks = -(-W // D) * -(-H // D)
+    blur = KM * 2 * (2 * R + 1)
+    solve = Q ** 3 / 3 + 3 * Q * Q + 12 * Q + 3 * NS
+    return blocks * 2 * (blur + solve)
+
+
+KERNEL_FLOPS = {  # fp64-bound kernels
+    "k_blur_solve_tile": k2_flops_per_frame,
+    "k_blur_solve": k2_flops_per_frame,
+}
+# DP peak from the unit count: 148 SMs x 64 FP64 FMA/clk (measured 63/clk/SM with a DFMA
+# microbenchmark, tools/ubench_fma.cu) x 2 flops x 1.965 GHz
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
 def load_peaks():
@@ -486,9 +511,25 @@ def run_flr(args, cfg, rank, world, local_rank):
                     "frac": ach / peak, "traffic": ncu_traffic(dom, args.config),
                     "algorithmic_bytes_per_launch": alg, "avg_launch_us": known[dom] * 1e3,
                     "peak_source": peak_src}
+        elif dom in KERNEL_FLOPS:
+            ach = KERNEL_FLOPS[dom](cfg) * F / (known[dom] * 1e-3) / 1e12
+            roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s (fp64)", "frac": ach / FP64_PEAK_TFLOPS, "traffic": ncu_traffic(dom, args.config),
+                    "avg_launch_us": known[dom] * 1e3, "peak_source": "derived: 148 SM x 64 DFMA/clk x 1.965 GHz"}
         else:
             roof = {"bound": "alu", "kernel": dom, "achieved": None, "peak": None, "unit": None, "frac": None,
                     "traffic": None, "avg_launch_us": known[dom] * 1e3}
+    # every kernel against its own roof (bytes for the streaming kernels, fp64 flops for K2)
+    kroof = {}
+    for n, t in known.items():
+        if n in KERNEL_BYTES:
+            a_ = KERNEL_BYTES[n](cfg) * F / (t * 1e-3) / 1e9
+            kroof[n] = {"bound": "hbm", "achieved": a_, "peak": peak, "unit": "GB/s", "frac": a_ / peak,
+                        "avg_launch_us": t * 1e3}
+        elif n in KERNEL_FLOPS:
+            a_ = KERNEL_FLOPS[n](cfg) * F / (t * 1e-3) / 1e12
+            kroof[n] = {"bound": "alu", "achieved": a_, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s (fp64)",
+                        "frac": a_ / FP64_PEAK_TFLOPS, "avg_launch_us": t * 1e3}
     step_ms = ms_max / K
     step_bytes = min_bytes_per_frame(cfg) * F
     step_roof = {"min_bytes_per_step": step_bytes, "achieved": step_bytes / (step_ms * 1e-3) / 1e9,
@@ -510,6 +551,7 @@ def run_flr(args, cfg, rank, world, local_rank):
                    "numerics": "fp32 streams, fp64 block blur+solve"},
         "roofline": roof, "step_roofline": step_roof,
         "kernel_us": {n: (t * 1e3 if t else None) for n, t in avg_ms.items()},
+        "kernel_roofline": kroof,
         "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": launches_per_step * K,
         "clocks": clocks,
         "checksums": allcs,

@@ -21,9 +21,15 @@ constexpr int kApplyWsM = 2;   // model stages per consumer
 template <int Q>
 struct ApplyWsCfg {
     using SD = StreamDims<Q>;
-    static constexpr int NC = kApplyWsNC, S = kApplyWsS, SM = kApplyWsM, THREADS = (NC + 1) * 32;
     static constexpr int ROWF = Q * kSeg;                 // floats per guide-row stage
     static constexpr int MODF = 2 * kApplyNCol * SD::MS;  // floats per model stage
+    // as many guide-row stages (<= kApplyWsS) as fit in 227 KB with 7 consumers
+    static constexpr int fit_stages(int s)
+    {
+        return (s <= 2 || (size_t)kApplyWsNC * ((s * ROWF + kApplyWsM * MODF + 31) / 32 * 32) * 4 + 4096 <= 232448)
+                   ? s : fit_stages(s - 1);
+    }
+    static constexpr int NC = kApplyWsNC, S = fit_stages(kApplyWsS), SM = kApplyWsM, THREADS = (NC + 1) * 32;
     static constexpr int WARPF = (S * ROWF + SM * MODF + 31) / 32 * 32;  // 128-byte aligned regions
     static constexpr size_t BAR_OFF = (size_t)NC * WARPF * sizeof(float);
     static constexpr int NBAR = 2 * (S + SM);  // full + empty per stage

@@ -22,10 +22,16 @@ constexpr int kFitWsS = 4;   // ring stages per consumer
 
 template <int Q>
 struct FitWsCfg {
-    static constexpr int NC = kFitWsNC, S = kFitWsS, THREADS = (NC + 1) * 32;
     static constexpr int STG = StreamDims<Q>::STG_FIT;  // floats per stage (one pixel row)
+    // as many stages (<= kFitWsS) as fit in 227 KB with 7 consumers
+    static constexpr int fit_stages(int s)
+    {
+        return (s <= 2 || (size_t)kFitWsNC * s * STG * 4 + 4096 <= 232448) ? s : fit_stages(s - 1);
+    }
+    static constexpr int NC = kFitWsNC, S = fit_stages(kFitWsS), THREADS = (NC + 1) * 32;
     static constexpr size_t BAR_OFF = (size_t)NC * S * STG * sizeof(float);
     static constexpr size_t SMEM = BAR_OFF + 2 * NC * S * sizeof(uint64_t);
+    static_assert(SMEM <= 232448, "fit pipeline exceeds 227 KB of shared memory");
 };
 
 // per-lane accumulators of one item, pixel-pair packed
@@ -78,7 +84,7 @@ template <int Q, int D, bool EDGE>
 __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], const float* ring, uint64_t* full,
                                             uint64_t* empty, int& k, int rows, int lane, int lb0, int x0, int W)
 {
-    constexpr int S = kFitWsS, STG = FitWsCfg<Q>::STG;
+    constexpr int S = FitWsCfg<Q>::S, STG = FitWsCfg<Q>::STG;
     {  // the block shift c = its top-left pixel (first row of the item)
         mbar_wait(&full[k % S], (k / S) & 1);
         const float* st = ring + (k % S) * STG;

@@ -153,7 +153,9 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     static const bool rows = std::getenv("FLR_ROWS_SOLVE") != nullptr;
     (void)NGRP;
     bool k2tile = false;
-    if (!tile && !rows && R >= 1 && R <= kTileMaxR && mstride == Dims<Q>::MSTRIDE) {
+    // the tile kernel keeps all KM blurred components of a block in registers: up to Q = 8
+    // (KM = 72); larger Q take the row variant (components in shared memory)
+    if (Q <= 8 && !tile && !rows && R >= 1 && R <= kTileMaxR && mstride == Dims<Q>::MSTRIDE) {
         // default: one tile kernel, moment field read once (+ halo) by TMA, no blurred-field
         // round trip through L2
         const dim3 grid(cdiv(Bx, kK2TX), cdiv(By, kK2TY), n);
