@@ -13,12 +13,15 @@
 // added once per item.  Sums are taken about the block's top-left pixel c (design rule
 // H1) and un-shifted to fp64 in the epilogue (FitAcc::store's algebra).
 #pragma once
-#include "flr_stream.cuh"
+#include "flr_persist.cuh"
 
 namespace flr {
 
 constexpr int kFitWsNC = 7;  // consumer warps (+1 producer = 8 warps: 2 per SMSP keeps the 255-register cap)
-constexpr int kFitWsS = 4;   // ring stages per consumer
+#ifndef FLR_FITWS_S
+#define FLR_FITWS_S 4
+#endif
+constexpr int kFitWsS = FLR_FITWS_S;  // ring stages per consumer
 
 template <int Q>
 struct FitWsCfg {
