@@ -53,8 +53,11 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __
     }
     __syncthreads();
     const int per_frame = a.nband * a.nsub * a.nseg, nitems = n * per_frame, GW = gridDim.x * NC;
+    // Only the producer touches data of earlier grids (the models, by bulk copy), so only it
+    // waits (griddepcontrol.wait), and only after it has queued the first guide rows: the
+    // guides are inputs of the call, complete before the fit grid got past its own wait
+    // (every grid of the chain triggers its dependents only after its wait).
     pdl_trigger();
-    pdl_wait();  // the models come from the previous grid
 
     auto geom = [&](int it, int& f) {
         f = it / per_frame;
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __
         uint64_t* mfull = rempty + S;
         uint64_t* mempty = mfull + SM;
         const uint64_t pg = policy_evict_first(), pm = policy_evict_normal();
-        int it = blockIdx.x * NC + c, f = 0, y = 0, kr = 0, km = 0;
+        int it = blockIdx.x * NC + c, f = 0, y = 0, kr = 0, km = 0, pre = 0;
         ApplyGeom g;
         bool need_models = true;
         auto next_item = [&]() {  // skip empty sub-bands (rows outside the image)
@@ -86,6 +89,15 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __
             need_models = true;
         };
         next_item();
+        {  // guide rows of the first item, ahead of the models (and of the wait)
+            int pit = it, py0 = y;
+            for (; kr < S && pit < nitems && py0 < g.y1; ++kr, ++py0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                apply_issue_row<Q>(a, g, f, py0, rows_st + kr * C::ROWF, &rfull[kr], pg);
+            }
+            pre = kr;
+        }
+        pdl_wait();  // the models come from the previous grid
         constexpr unsigned mask = (1u << NC) - 1;
         while (__any_sync(mask, it < nitems)) {
             if (it >= nitems) continue;
@@ -96,6 +108,13 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __
                     apply_issue_models<Q>(a, g, f, mod_st + s * C::MODF, &mfull[s], pm);
                     ++km;
                     need_models = false;
+                }
+            } else if (pre > 0) {  // rows of the first item already queued before the wait
+                y += pre;
+                pre = 0;
+                if (y >= g.y1) {
+                    it += GW;
+                    next_item();
                 }
             } else {
                 const int s = kr % S;

@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(FitWsCfg<Q>::THREADS, 1) k_fit_ws(const __grid
     }
     __syncthreads();
     const int per_frame = a.By * a.nseg, nitems = n * per_frame, GW = gridDim.x * NC;
-    pdl_trigger();
     pdl_wait();  // caller data may come from the previous grid
+    pdl_trigger();  // dependents launch only once we are past our own wait
 
     if (warp == NC) {
         // ---------------- producer: lane c feeds consumer c ----------------

@@ -243,7 +243,7 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
                 a.nsub *= 2;
             if (const char* e = std::getenv("FLR_APPLY_NSUB")) a.nsub = std::max(1, std::atoi(e));
             if (D % a.nsub) a.nsub = 1;
-            a.ready = ctx.wave_k2, a.ready_target = ctx.wave_target, a.nrt = ctx.wave_nrt;
+            a.ready = ctx.wave_k2, a.ready_target = ctx.wave_target, a.nrt = ctx.wave_nrt, a.ready_ty = kK2TY;
             ctx.wave_k2 = nullptr;
             const int items = n * a.nseg * a.nband * a.nsub;
             // many items (batches): the 11-warp self-feeding rings keep more rows in flight;

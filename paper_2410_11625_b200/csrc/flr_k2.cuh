@@ -21,7 +21,11 @@
 
 namespace flr {
 
-constexpr int kK2TX = 32, kK2TY = 8, kK2Threads = kK2TX * kK2TY;
+#ifndef FLR_K2_TY
+#define FLR_K2_TY 8
+#endif
+constexpr int kK2TX = 32, kK2TY = FLR_K2_TY, kK2Threads = kK2TX * kK2TY;
+constexpr int kK2MinBlocks = kK2TY <= 4 ? 2 : 1;  // CTAs per SM the register budget allows
 
 template <int Q, int R>
 struct K2Geom {
@@ -54,7 +58,7 @@ struct K2Geom {
 
 // tm: the fp64 moment field [n*KM][By][Bxp] with box {HX, TY + 2R, G} (K2Geom)
 template <int Q, int R>
-__global__ void __launch_bounds__(kK2Threads, 1)
+__global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
     k_blur_solve_tile(const __grid_constant__ CUtensorMap tm, int Bx, int By, float* __restrict__ models,
                       double eps_add, double eps_mul, const __grid_constant__ Taps t, const int* wait_rows,
                       int wait_target, int* signal)
@@ -80,10 +84,11 @@ __global__ void __launch_bounds__(kK2Threads, 1)
         for (int i = 0; i < S; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
     }
-    pdl_trigger();
     if (!wait_rows) {
         pdl_wait();  // the moment field comes from the previous grid
-    } else {  // wavefront: only the FIT rows this tile reads (+- R), one polling thread per row
+        pdl_trigger();  // dependents launch only once we are past our own wait
+    } else {
+        pdl_trigger();  // wavefront: wait only for the FIT rows this tile reads (+- R), one thread per row
         const int rr = by0 - R + tid;
         if (tid < TY + 2 * R && rr >= 0 && rr < By)
             while (ld_acquire(&wait_rows[f * By + rr]) < wait_target) __nanosleep(64);

@@ -116,8 +116,8 @@ struct ApplySeq {
     {
         if (it >= nitems) return false;
         if (row < 0) {
-            if (a->ready) {  // wavefront: the K2 tile rows (8 block rows each) holding rows j0, j1
-                const int m0 = g.j0 / 8, m1 = g.j1 / 8;
+            if (a->ready) {  // wavefront: the K2 tile rows (ready_ty block rows each) holding rows j0, j1
+                const int m0 = g.j0 / a->ready_ty, m1 = g.j1 / a->ready_ty;
                 const int v0 = ld_relaxed(&a->ready[f * a->nrt + m0]), v1 = ld_relaxed(&a->ready[f * a->nrt + m1]);
                 if (v0 < a->ready_target || v1 < a->ready_target) return false;  // retried from ring_wait
                 fence_acquire();
@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(FitCfg<Q>::THREADS, 1) k_fit_stream(const __gr
     seq.a = &a, seq.it = first, seq.nitems = nitems, seq.per_frame = per_frame, seq.step = GW;
     seq.pg = std_policy_guides_fit(), seq.py = policy_evict_first();
     seq.decode();
-    pdl_trigger();
     pdl_wait();  // caller data may come from the previous grid: wait before the first read
+    pdl_trigger();  // dependents launch only once we are past our own wait
     if (lane == 0) ring_fill(r, seq);
 #ifdef FLR_DBG_TIMES
     const long long tk0 = clock64();
@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(kFitLdgWarps * 32, 1) k_fit_ldg(const __grid_c
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int per_frame = a.By * a.nseg, nitems = n * per_frame;
     const int GW = gridDim.x * kFitLdgWarps;
-    pdl_trigger();
     pdl_wait();
+    pdl_trigger();  // dependents launch only once we are past our own wait
     for (int it = blockIdx.x * kFitLdgWarps + w; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it - f * per_frame, by = rem / a.nseg;
         fit_ldg_item<Q, D>(a, f, by, rem - by * a.nseg, lane);
@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(ApplyCfg<Q>::THREADS, 1) k_apply_stream(const 
     seq.a = &a, seq.it = first, seq.nitems = nitems, seq.per_frame = per_frame, seq.step = GW;
     seq.pg = policy_evict_first(), seq.pm = policy_evict_normal();  // last use of the guides
     seq.decode();
-    pdl_trigger();
     if (!a.ready) pdl_wait();  // models come from the previous grid (or per tile row, see ApplySeq)
+    pdl_trigger();
     if (lane == 0) ring_fill(r, seq);
     for (int it = first; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it % per_frame;

@@ -397,7 +397,7 @@ struct ApplyArgs {
     int W, H, D, Bx, By, nseg, nband;
     int nsub;  // sub-bands per band (D % nsub == 0): more, smaller APPLY items for one frame
     const int* ready;  // optional [n][nrt] K2 tile-row counters (complete at ready_target)
-    int ready_target, nrt;
+    int ready_target, nrt, ready_ty;  // ready_ty: block rows per counter
 };
 
 __host__ __device__ inline int apply_nband(int H, int D, int By)

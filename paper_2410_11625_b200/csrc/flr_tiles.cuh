@@ -410,8 +410,8 @@ __global__ void __launch_bounds__(kTileTX* kTileTY) k_blur_solve(const __grid_co
         mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
-    pdl_trigger();
     pdl_wait();  // the moment field comes from the previous grid
+    pdl_trigger();  // dependents launch only once we are past our own wait
     __syncthreads();
     unsigned use[2] = {0, 0};
     blur_solve_tile<Q, R>(&tm, blockIdx.z, blockIdx.x * kTileTX, blockIdx.y * kTileTY, Bx, By, models, mstride,
@@ -451,8 +451,8 @@ __global__ void __launch_bounds__(256) k_blur(const __grid_constant__ CUtensorMa
     uint64_t* bar = reinterpret_cast<uint64_t*>(vb + BG::VB);
     const int f = blockIdx.z / NGRP, grp = blockIdx.z - f * NGRP;
     const int bx0 = blockIdx.x * TX, by0 = blockIdx.y * TY, k0 = grp * kBlurG;
-    pdl_trigger();
     pdl_wait();  // the moment field comes from the previous grid
+    pdl_trigger();  // dependents launch only once we are past our own wait
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
@@ -541,8 +541,8 @@ __global__ void __launch_bounds__(kRowsThreads, 3) k_blur_rows(const double* __r
     const size_t ps = (size_t)By * Bxp;
     const double* src = mom + (size_t)blockIdx.y * ps;
     double* dst = out + (size_t)blockIdx.y * ps;
-    pdl_trigger();
     pdl_wait();  // the moment field comes from the previous grid
+    pdl_trigger();  // dependents launch only once we are past our own wait
 #ifdef FLR_DBG_PHASES
     long long ts0 = clock64(), gt0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
@@ -649,8 +649,8 @@ __global__ void __launch_bounds__(128) k_solve(int Bx, int Bxp, int By, const do
                                               double eps_mul)
 {
     const int bx = blockIdx.x * blockDim.x + threadIdx.x, by = blockIdx.y, f = blockIdx.z;
-    pdl_trigger();
     pdl_wait();  // the blurred field comes from the previous grid
+    pdl_trigger();  // dependents launch only once we are past our own wait
     if (bx >= Bx) return;
     const size_t cs = (size_t)By * Bxp;
     const double* src = blurred + (size_t)f * Dims<Q>::KM * cs + (size_t)by * Bxp + bx;
@@ -694,8 +694,8 @@ __global__ void __launch_bounds__(kSolveRowN, 3) k_solve_rows(int Bx, int Bxp, i
         mbar_init(&bar[1], 1);
         fence_mbar_init();
     }
-    pdl_trigger();
     pdl_wait();  // the blurred field comes from the previous grid
+    pdl_trigger();  // dependents launch only once we are past our own wait
     __syncthreads();
     const size_t cs = (size_t)By * Bxp;
     const double* src = blurred + (size_t)f * KM * cs + (size_t)by * Bxp + bx0;
