@@ -46,6 +46,7 @@ def lib():
         L.flr_ref_apply.argtypes = [i, i, i, i, i, i, i, dp, fp, dp]
         L.flr_ref_denoise.argtypes = [i, i, i, i, i, d, i, d, d, fp, fp, dp]
         L.flr_ref_denoise_upsample.argtypes = [i, i, i, i, i, i, d, i, d, d, fp, fp, fp, dp]
+        L.flr_ref_denoise_modulated.argtypes = [i, i, i, i, i, d, i, d, d, d, fp, fp, fp, fp, dp]
         L.flr_ref_num_threads.argtypes = []
         for name in ("flr_ref_moments", "flr_ref_gauss_taps", "flr_ref_blur", "flr_ref_solve_block",
                      "flr_ref_fit", "flr_ref_apply", "flr_ref_denoise", "flr_ref_denoise_upsample",
@@ -181,6 +182,29 @@ def denoise(guides, radiance, D=8, sigma=10.0, R=None, eps_add=1e-5, eps_mul=1e-
     out, op = _out((n, 3, H, W))
     _check(lib().flr_ref_denoise(n, Q, W, H, D, float(sigma), int(R), float(eps_add),
                                  float(eps_mul), gp, rp, op), "flr_ref_denoise")
+    return out
+
+
+def denoise_modulated(guides, radiance_mod, albedo, direct=None, D=8, sigma=10.0, R=None, eps_add=1e-5,
+                      eps_mul=1e-4, floor=1e-3):
+    """The paper's albedo protocol: out = A * FLR(guides, P / max(A, floor)) + direct."""
+    g, r = _frames(guides, radiance_mod)
+    a, _ = _frames(albedo)
+    n, Q, H, W = g.shape
+    assert a.shape == r.shape, "albedo must have the radiance's shape [n][3][H][W]"
+    if R is None:
+        R = default_radius(sigma, D)
+    g, gp = _f32(g)
+    r, rp = _f32(r)
+    a, ap = _f32(a)
+    dp_ = None
+    if direct is not None:
+        dd, _ = _frames(direct)
+        assert dd.shape == r.shape, "direct must have the radiance's shape [n][3][H][W]"
+        dd, dp_ = _f32(dd)
+    out, op = _out((n, 3, H, W))
+    _check(lib().flr_ref_denoise_modulated(n, Q, W, H, D, float(sigma), int(R), float(eps_add), float(eps_mul),
+                                           float(floor), gp, rp, ap, dp_, op), "flr_ref_denoise_modulated")
     return out
 
 

@@ -46,12 +46,12 @@ int flr_ref_num_threads(void)
  *   x~_p = [1, X_p,1 .. X_p,Q] (the first guide column is all ones).
  * The box filter is a SUM (R12); edge blocks are truncated (R5).
  * ------------------------------------------------------------------------- */
-int flr_ref_moments(int n, int Q, int W, int H, int D,
-                    const float* guides, const float* radiance,
-                    double* M, double* N)
+/* block sums; the radiance is given either as float (radiance) or as double (radiance_d) */
+static int moments_impl(int n, int Q, int W, int H, int D, const float* guides,
+                        const float* radiance, const double* radiance_d, double* M, double* N)
 {
     if (n < 1 || Q < 1 || Q > MAXP - 1 || W < 1 || H < 1 || D < 1 || !guides ||
-        !radiance || !M || !N)
+        !(radiance || radiance_d) || !M || !N)
         return 1;
     const int P = Q + 1;
     const int Bx = ceil_div(W, D), By = ceil_div(H, D);
@@ -68,7 +68,7 @@ int flr_ref_moments(int n, int Q, int W, int H, int D,
         for (int i = 0; i < P * P; ++i) Mb[i] = 0.0;
         for (int i = 0; i < P * 3; ++i) Nb[i] = 0.0;
         const float* G = guides + (long)f * Q * plane;
-        const float* Y = radiance + (long)f * 3 * plane;
+        const long yoff = (long)f * 3 * plane;
         const int y1 = (by + 1) * D < H ? (by + 1) * D : H;
         const int x1 = (bx + 1) * D < W ? (bx + 1) * D : W;
         for (int y = by * D; y < y1; ++y)
@@ -78,7 +78,8 @@ int flr_ref_moments(int n, int Q, int W, int H, int D,
                 double yv[3];
                 xt[0] = 1.0;
                 for (int q = 0; q < Q; ++q) xt[1 + q] = (double)G[q * plane + p];
-                for (int c = 0; c < 3; ++c) yv[c] = (double)Y[c * plane + p];
+                for (int c = 0; c < 3; ++c)
+                    yv[c] = radiance ? (double)radiance[yoff + c * plane + p] : radiance_d[yoff + c * plane + p];
                 for (int i = 0; i < P; ++i)
                     for (int j = 0; j < P; ++j) Mb[i * P + j] += xt[i] * xt[j];
                 for (int i = 0; i < P; ++i)
@@ -86,6 +87,13 @@ int flr_ref_moments(int n, int Q, int W, int H, int D,
             }
     }
     return 0;
+}
+
+int flr_ref_moments(int n, int Q, int W, int H, int D,
+                    const float* guides, const float* radiance,
+                    double* M, double* N)
+{
+    return radiance ? moments_impl(n, Q, W, H, D, guides, radiance, NULL, M, N) : 1;
 }
 
 /* Gaussian window taps: unnormalised, peak 1 (R2). */
@@ -243,13 +251,13 @@ int flr_ref_solve_block(int P, const double* M, const double* N,
     return 0;
 }
 
-int flr_ref_fit(int n, int Q, int W, int H, int D_fit, int U,
-                double sigma, int R, double eps_add, double eps_mul,
-                const float* guides, const float* radiance, double* A)
+static int fit_impl(int n, int Q, int W, int H, int D_fit, int U, double sigma, int R,
+                    double eps_add, double eps_mul, const float* guides, const float* radiance,
+                    const double* radiance_d, double* A)
 {
     if (n < 1 || Q < 1 || Q > MAXP - 1 || W < 1 || H < 1 || D_fit < 1 || U < 1 ||
         !(sigma > 0.0) || R < 0 || !(eps_add >= 0.0) || !(eps_mul >= 0.0) ||
-        !(eps_mul < 1.0) || !guides || !radiance || !A)
+        !(eps_mul < 1.0) || !guides || !(radiance || radiance_d) || !A)
         return 1;
     const int P = Q + 1;
     const int Bx = ceil_div(W, D_fit), By = ceil_div(H, D_fit);
@@ -260,7 +268,7 @@ int flr_ref_fit(int n, int Q, int W, int H, int D_fit, int U,
     double* Nb = (double*)malloc(sizeof(double) * nblk * P * 3);
     int rc = 1;
     if (!M || !N || !Mb || !Nb) goto done;
-    if ((rc = flr_ref_moments(n, Q, W, H, D_fit, guides, radiance, M, N))) goto done;
+    if ((rc = moments_impl(n, Q, W, H, D_fit, guides, radiance, radiance_d, M, N))) goto done;
     /* blur std in blocks: sigma (output pixels) / block size in output pixels */
     if ((rc = flr_ref_blur(n, P, Bx, By, sigma / ((double)D_fit * U), R, M, N, Mb, Nb)))
         goto done;
@@ -276,6 +284,14 @@ done:
     free(Mb);
     free(Nb);
     return rc;
+}
+
+int flr_ref_fit(int n, int Q, int W, int H, int D_fit, int U,
+                double sigma, int R, double eps_add, double eps_mul,
+                const float* guides, const float* radiance, double* A)
+{
+    if (!radiance) return 1;
+    return fit_impl(n, Q, W, H, D_fit, U, sigma, R, eps_add, eps_mul, guides, radiance, NULL, A);
 }
 
 /* ---------------------------------------------------------------------------
@@ -361,6 +377,42 @@ int flr_ref_denoise_upsample(int n, int Q, int W_lo, int H_lo, int D_fit, int U,
     int rc = flr_ref_fit(n, Q, W_lo, H_lo, D_fit, U, sigma, R, eps_add, eps_mul, guides_lo,
                          radiance_lo, A);
     if (!rc) rc = flr_ref_apply(n, Q, W_lo * U, H_lo * U, D_fit * U, Bx, By, A, guides_hi, out);
+    free(A);
+    return rc;
+}
+
+/* The paper's input/output protocol around FLR:
+ *   y   = P / max(A, floor)          per pixel and channel (demodulate; floor: R20)
+ *   I   = FLR(guides, y)             fit + apply in fp64 as above
+ *   out = A * I (+ direct)           remodulate with the unfloored albedo, then add the
+ *                                    noise-free direct radiance if given (R21)
+ * The demodulated radiance is kept in double (never rounded to float). */
+int flr_ref_denoise_modulated(int n, int Q, int W, int H, int D, double sigma, int R,
+                              double eps_add, double eps_mul, double floor,
+                              const float* guides, const float* radiance_mod, const float* albedo,
+                              const float* direct, double* out)
+{
+    if (n < 1 || Q < 1 || Q > MAXP - 1 || W < 1 || H < 1 || D < 1 || !(floor > 0.0) ||
+        !guides || !radiance_mod || !albedo || !out)
+        return 1;
+    const long total = (long)n * 3 * W * H;
+    const int P = Q + 1;
+    const int Bx = ceil_div(W, D), By = ceil_div(H, D);
+    double* y = (double*)malloc(sizeof(double) * total);
+    double* A = (double*)malloc(sizeof(double) * (long)n * By * Bx * P * 3);
+    int rc = 1;
+    if (!y || !A) goto done;
+    for (long i = 0; i < total; ++i) {
+        const double a = (double)albedo[i];
+        y[i] = (double)radiance_mod[i] / (a > floor ? a : floor);
+    }
+    rc = fit_impl(n, Q, W, H, D, 1, sigma, R, eps_add, eps_mul, guides, NULL, y, A);
+    if (!rc) rc = flr_ref_apply(n, Q, W, H, D, Bx, By, A, guides, out);
+    if (!rc)
+        for (long i = 0; i < total; ++i)
+            out[i] = (double)albedo[i] * out[i] + (direct ? (double)direct[i] : 0.0);
+done:
+    free(y);
     free(A);
     return rc;
 }

@@ -13,6 +13,7 @@
  *         -> appendix normalise + regularise + solve per block
  *   apply = bilinear blend of the per-block models, then I = x A
  *   joint denoise+upsample: fit at low resolution, apply with hi-res guides
+ *   albedo protocol: demodulate, denoise, remodulate, add direct light
  * Readings of ambiguous passages (R1..R19) are listed in DESIGN.md section 3.
  *
  * Conventions (all arrays row-major, C order, host memory, caller-owned):
@@ -77,6 +78,15 @@ int flr_ref_denoise_upsample(int n, int Q, int W_lo, int H_lo, int D_fit, int U,
                              double sigma, int R, double eps_add, double eps_mul,
                              const float* guides_lo, const float* radiance_lo,
                              const float* guides_hi, double* out);
+
+/* The paper's protocol around FLR: radiance_mod = albedo-modulated
+ * noisy indirect lighting, albedo [n][3][H][W]; y = radiance_mod / max(albedo, floor),
+ * I = denoise(guides, y), out = albedo * I + direct (direct may be NULL = zero).
+ * Readings R20 (floor) and R21 (direct composite) in DESIGN.md. */
+int flr_ref_denoise_modulated(int n, int Q, int W, int H, int D, double sigma, int R,
+                              double eps_add, double eps_mul, double floor,
+                              const float* guides, const float* radiance_mod,
+                              const float* albedo, const float* direct, double* out);
 
 /* Number of OpenMP threads the oracle will use (1 when built without OpenMP). */
 int flr_ref_num_threads(void);

@@ -349,6 +349,61 @@ def test_p12_affine_field_exact_across_resolutions(oracle_mod):
     np.testing.assert_allclose(out, ref, atol=2e-5)
 
 
+# ---------------------------------------------------------------- P13: albedo protocol
+# "we divide P by A, denoise, then multiply again with A";
+# the direct light is noise-free and added back.  Readings R20 (albedo floor
+# 1e-3 in the division only) and R21 (direct added after remodulation) in DESIGN.md.
+def test_p13_unit_albedo_is_plain_denoise(oracle_mod):
+    rng = np.random.default_rng(50)
+    G, Y = _scene(rng)
+    A = np.ones_like(Y)
+    np.testing.assert_array_equal(oracle_mod.denoise_modulated(G, Y, A, D=4, sigma=10.0, R=3),
+                                  oracle_mod.denoise(G, Y, D=4, sigma=10.0, R=3))
+
+
+def test_p13_modulated_constant_lighting_is_reproduced(oracle_mod):
+    """P = A * L with constant lighting L: demodulation gives L everywhere, FLR maps a
+    constant to itself (P7), remodulation gives back P."""
+    rng = np.random.default_rng(51)
+    G, _ = _scene(rng)
+    H, W = G.shape[1:]
+    L = np.array([0.3, 1.7, 0.05])[:, None, None]
+    A = rand_planes(rng, 3, H, W, 0.05, 1.0)
+    P = (A.astype(np.float64) * L).astype(np.float32)
+    out = oracle_mod.denoise_modulated(G, P, A, D=4, sigma=8.0, R=2)[0]
+    np.testing.assert_allclose(out, A.astype(np.float64) * L, rtol=1e-6, atol=1e-9)
+
+
+def test_p13_floor_and_remodulation_by_hand(oracle_mod):
+    """Against the composition written out with numpy and the plain oracle: the floor
+    only guards the division, the remodulation uses the raw albedo (zero albedo gives
+    zero output), and the direct light is added last."""
+    rng = np.random.default_rng(52)
+    G, Y = _scene(rng)
+    A = rand_planes(rng, 3, *Y.shape[1:], 0.0, 1.0)
+    A[:, :5, :7] = 0.0             # below the floor: divide by 1e-3
+    A[1, 10:12, :] = 5e-4
+    Dl = rand_planes(rng, 3, *Y.shape[1:], 0.0, 2.0)
+    floor = 1e-3
+    y = Y.astype(np.float64) / np.maximum(A.astype(np.float64), floor)
+    I = oracle_mod.denoise(G, y.astype(np.float32), D=4, sigma=10.0, R=3)[0]
+    ref = A.astype(np.float64) * I + Dl.astype(np.float64)
+    out = oracle_mod.denoise_modulated(G, Y, A, Dl, D=4, sigma=10.0, R=3, floor=floor)[0]
+    # y is rounded to float for the plain oracle: relative 1e-7 differences
+    np.testing.assert_allclose(out, ref, rtol=2e-5, atol=1e-6)
+    assert np.array_equal(out[:, :5, :7], Dl[:, :5, :7].astype(np.float64))
+
+
+def test_p13_direct_light_is_additive(oracle_mod):
+    rng = np.random.default_rng(53)
+    G, Y = _scene(rng)
+    A = rand_planes(rng, 3, *Y.shape[1:], 0.05, 1.0)
+    Dl = rand_planes(rng, 3, *Y.shape[1:], 0.0, 3.0)
+    a = oracle_mod.denoise_modulated(G, Y, A, Dl, D=4, sigma=10.0, R=3)
+    b = oracle_mod.denoise_modulated(G, Y, A, None, D=4, sigma=10.0, R=3)
+    np.testing.assert_allclose(a - b, Dl[None].astype(np.float64), rtol=0, atol=1e-12)
+
+
 # ---------------------------------------------------------------- argument errors
 def test_oracle_rejects_bad_arguments(oracle_mod):
     G = np.zeros((1, 4, 4), dtype=np.float32)
