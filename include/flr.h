@@ -131,6 +131,25 @@ flr_status flr_denoise_upsample(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo
                                 const flr_params* p, float* out, void* workspace,
                                 size_t workspace_bytes, flr_stream_t stream);
 
+/* The paper's protocol around FLR: the renderer's indirect
+ * radiance is albedo-modulated, FLR denoises the DEMODULATED signal, and the result is
+ * remodulated and the noise-free direct light added:
+ *   y   = radiance_mod / max(albedo, albedo_floor)      per pixel and channel (R20)
+ *   I   = flr_denoise(guides, y)                         (p->upsample must be 1)
+ *   out = albedo * I + direct                            (R21; direct == NULL means zero)
+ * radiance_mod, albedo, direct, out: [n][3][H][W] device planes; guides [n][Q][H][W].
+ * albedo_floor > 0 (finite) only guards the division (SPEC's 1e-3 convention).
+ * When W % 4 == 0, the planes are 16-byte aligned and p->block is 4, 8 or 16 the
+ * demodulation runs inside the moment kernel's loads and (for block 8/16) the
+ * remodulation inside the apply kernel's stores; any other shape runs two extra
+ * elementwise kernels (the demodulated radiance is staged in `out`).  Same workspace as
+ * flr_denoise.  Errors as flr_denoise; FLR_ERR_INVALID_VALUE for a NULL albedo or a
+ * non-positive floor. */
+flr_status flr_denoise_modulated(int32_t n, int32_t Q, int32_t W, int32_t H, const float* guides,
+                                 const float* radiance_mod, const float* albedo, const float* direct,
+                                 float albedo_floor, const flr_params* p, float* out, void* workspace,
+                                 size_t workspace_bytes, flr_stream_t stream);
+
 /* Optional per-launch timing for benchmarks.  `events` holds `capacity`
  * caller-created cudaEvent_t handles (create them with timing enabled).  The
  * traced calls record events[i] on `stream` immediately before their i-th
@@ -155,6 +174,10 @@ flr_status flr_denoise_upsample_traced(int32_t n, int32_t Q, int32_t W_lo, int32
                                        const flr_params* p, float* out, void* workspace,
                                        size_t workspace_bytes, flr_stream_t stream,
                                        flr_event_trace* trace);
+flr_status flr_denoise_modulated_traced(int32_t n, int32_t Q, int32_t W, int32_t H, const float* guides,
+                                        const float* radiance_mod, const float* albedo, const float* direct,
+                                        float albedo_floor, const flr_params* p, float* out, void* workspace,
+                                        size_t workspace_bytes, flr_stream_t stream, flr_event_trace* trace);
 
 /* Number of kernel launches the last successful call on this thread enqueued
  * (bench accounting; thread-local, not part of the computation). */

@@ -19,7 +19,7 @@ import math
 import os
 
 __all__ = ["FLRError", "Params", "lib", "lib_path", "workspace_size", "effective_radius", "fit",
-           "apply", "denoise", "denoise_upsample", "Denoiser", "EventTrace", "last_launch_count", "last_launch_names",
+           "apply", "denoise", "denoise_upsample", "denoise_modulated", "Denoiser", "EventTrace", "last_launch_count", "last_launch_names",
            "VARIANT_AUTO", "VARIANT_STAGED", "VARIANT_FUSED"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -95,12 +95,17 @@ def lib():
         L.flr_denoise_traced.argtypes = [i32, i32, i32, i32, dp, dp, pp, dp, vp, sz, vp, tp]
         L.flr_denoise_upsample_traced.argtypes = [i32, i32, i32, i32, dp, dp, i32, i32, dp, pp, dp, vp, sz,
                                                   vp, tp]
+        L.flr_denoise_modulated.argtypes = [i32, i32, i32, i32, dp, dp, dp, dp, ctypes.c_float, pp, dp, vp, sz,
+                                            vp]
+        L.flr_denoise_modulated_traced.argtypes = [i32, i32, i32, i32, dp, dp, dp, dp, ctypes.c_float, pp, dp,
+                                                   vp, sz, vp, tp]
         L.flr_last_launch_count.argtypes = []
         L.flr_last_launch_count.restype = i32
         L.flr_last_launch_name.argtypes = [i32]
         L.flr_last_launch_name.restype = ctypes.c_char_p
         for f in ("flr_workspace_size", "flr_fit", "flr_apply", "flr_denoise", "flr_denoise_upsample",
-                  "flr_denoise_traced", "flr_denoise_upsample_traced"):
+                  "flr_denoise_traced", "flr_denoise_upsample_traced", "flr_denoise_modulated",
+                  "flr_denoise_modulated_traced"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -263,6 +268,32 @@ def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, 
     _check(lib().flr_denoise_upsample(n, Q, W, H, _ptr(g), _ptr(y), Wh, Hh, _ptr(gh), ctypes.byref(p),
                                       _ptr(out), _ptr(ws), ws.numel() * ws.element_size(),
                                       _stream_ptr(g.device)), "flr_denoise_upsample")
+    return out
+
+
+def denoise_modulated(guides, radiance_mod, albedo, direct=None, *, block=8, sigma=10.0, radius=0,
+                      eps_add=1e-5, eps_mul=1e-4, albedo_floor=1e-3, out=None, workspace=None):
+    """The paper's protocol: demodulate by max(albedo, floor), FLR-denoise,
+    remodulate, add the direct light.  All radiance-like tensors are [n,3,H,W]."""
+    torch = _torch()
+    g = _frames(guides, "guides")
+    r = _frames(radiance_mod, "radiance_mod", 3)
+    a = _frames(albedo, "albedo", 3)
+    d = _frames(direct, "direct", 3) if direct is not None else None
+    n, Q, H, W = g.shape
+    for t, nm in ((r, "radiance_mod"), (a, "albedo")) + (((d, "direct"),) if d is not None else ()):
+        if tuple(t.shape) != (n, 3, H, W):
+            raise ValueError(f"{nm} must be [n,3,H,W] matching guides")
+    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, VARIANT_AUTO)
+    if out is None:
+        out = torch.empty((n, 3, H, W), dtype=torch.float32, device=g.device)
+    ws_bytes = workspace_size(n, Q, W, H, block=block, sigma=sigma, radius=radius, eps_add=eps_add,
+                              eps_mul=eps_mul)
+    ws = _workspace(ws_bytes, g.device, workspace)
+    _check(lib().flr_denoise_modulated(n, Q, W, H, _ptr(g), _ptr(r), _ptr(a), _ptr(d) if d is not None else None,
+                                       float(albedo_floor), ctypes.byref(p), _ptr(out), _ptr(ws),
+                                       ws.numel() * ws.element_size(), _stream_ptr(g.device)),
+           "flr_denoise_modulated")
     return out
 
 

@@ -11,6 +11,7 @@ from __future__ import annotations
 import argparse
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -46,13 +47,35 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
+def _digest(src, deps, defines):
+    """Content hash of a unit's inputs: an object is rebuilt whenever what it was compiled
+    from differs (mtimes alone miss edits made while a build was running)."""
+    h = hashlib.sha1()
+    for f in [src] + sorted(deps):
+        with open(f, "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    h.update(" ".join(NVFLAGS + list(defines)).encode())
+    return h.hexdigest()
+
+
+def _unit_stale(obj, src, deps, defines):
+    try:
+        with open(obj + ".sha") as fh:
+            return fh.read().strip() != _digest(src, deps, defines) or not os.path.exists(obj)
+    except OSError:
+        return True
+
+
 def _compile(src, obj, defines=(), verbose=False):
+    digest = _digest(src, _deps(), defines)  # of the inputs as they are when compilation starts
     cmd = [_nvcc()] + NVFLAGS + list(defines) + ["-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {os.path.basename(src)}:\n{r.stdout}\n{r.stderr}")
+    with open(obj + ".sha", "w") as fh:
+        fh.write(digest)
     return obj
 
 
@@ -70,7 +93,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         stub = () if q in keep else ("-DFLR_STUB",)
         tag = "" if q in keep else "_stub"
         units.append((inst, os.path.join(OBJ, f"flr_inst_q{q}{tag}.o"), (f"-DFLR_Q={q}",) + stub))
-    todo = [u for u in units if force or _stale(u[1], [u[0]] + deps)]
+    todo = [u for u in units if force or _unit_stale(u[1], u[0], deps, u[2])]
     if todo:
         jobs = jobs or max(1, min(len(todo), os.cpu_count() or 1))
         with cf.ThreadPoolExecutor(jobs) as ex:

@@ -159,6 +159,26 @@ flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, co
     return FLR_OK;
 }
 
+// generic (unfused) albedo protocol, any shape: y = r / max(a, floor) into `y`, and
+// out = a * out + d in place (R20, R21)
+__global__ void k_demod(size_t total, const float* __restrict__ r, const float* __restrict__ a, float afloor,
+                        float* __restrict__ y)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x)
+        y[i] = r[i] * __frcp_rn(fmaxf(a[i], afloor));
+}
+__global__ void k_remod(size_t total, float* __restrict__ out, const float* __restrict__ a,
+                        const float* __restrict__ d)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = fmaf(a[i], out[i], d ? d[i] : 0.0f);
+}
+inline unsigned ew_grid(size_t total)
+{
+    const size_t b = (total + 255) / 256;
+    return (unsigned)(b < 148 * 16 ? b : 148 * 16);
+}
+
 flr_status check_ws(int n, int Q, int W, int H, const flr_params* p, void* ws, size_t bytes)
 {
     size_t need = 0;
@@ -315,6 +335,57 @@ flr_status flr_denoise_traced(int32_t n, int32_t Q, int32_t W, int32_t H, const 
     if (p && p->upsample != 1) return FLR_ERR_INVALID_VALUE;
     return flr_denoise_upsample_traced(n, Q, W, H, guides, radiance, W, H, guides, p, out, workspace,
                                        workspace_bytes, stream, trace);
+}
+
+flr_status flr_denoise_modulated_traced(int32_t n, int32_t Q, int32_t W, int32_t H, const float* guides,
+                                        const float* radiance_mod, const float* albedo, const float* direct,
+                                        float albedo_floor, const flr_params* p, float* out, void* workspace,
+                                        size_t workspace_bytes, flr_stream_t stream, flr_event_trace* trace)
+{
+    flr_status st = check_fit_args(n, Q, W, H, guides, radiance_mod, p);
+    if (st) return st;
+    if (p->upsample != 1) return FLR_ERR_INVALID_VALUE;
+    if (!albedo || !out || !(albedo_floor > 0.0f) || !std::isfinite(albedo_floor)) return FLR_ERR_INVALID_VALUE;
+    if (!aligned(albedo, 4) || !aligned(out, 4) || (direct && !aligned(direct, 4))) return FLR_ERR_ALIGNMENT;
+    if ((st = check_ws(n, Q, W, H, p, workspace, workspace_bytes))) return st;
+    const int D = p->block;
+    const int Bx = cdiv(W, D), By = cdiv(H, D);
+    const Layout L = layout(n, Q, Bx, By);
+    float* models = (float*)((char*)workspace + L.models);
+    const int ms = mstride_of(Q);
+    const size_t total = (size_t)n * 3 * W * H;
+    LaunchCtx ctx = make_ctx(stream, trace);
+    if (fit_mod_fused(D, W, guides, radiance_mod, albedo)) {  // demodulation in the moment kernel's loads
+        const double sblk = p->sigma / (double)D;
+        const Taps taps = make_taps(sblk, effective_radius(p));
+        char* base = (char*)workspace;
+        FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, guides, radiance_mod, (float*)(base + L.raw),
+                                          (double*)(base + L.mom), (double*)(base + L.hb), models, ms,
+                                          p->eps_add, p->eps_mul, taps, ctx, albedo, albedo_floor)));
+    } else {  // demodulate into `out` (same shape), then the plain fit reads it
+        ctx.before("k_demod");
+        k_demod<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(total, radiance_mod, albedo, albedo_floor, out);
+        if ((st = do_fit(n, Q, W, H, guides, out, p, models, ms, workspace, ctx))) return st;
+    }
+    bool mod_ok = false;
+    FLR_DISPATCH_Q(Q, (mod_ok = apply_mod_supported<QQ>()));
+    if (mod_ok && apply_mod_fused(D, W, models, guides, out, albedo, direct)) {  // remodulation in the apply's stores
+        FLR_DISPATCH_Q(Q, (launch_apply<QQ>(n, W, H, D, Bx, By, models, ms, guides, out, ctx, albedo, direct)));
+    } else {
+        FLR_DISPATCH_Q(Q, (launch_apply<QQ>(n, W, H, D, Bx, By, models, ms, guides, out, ctx)));
+        ctx.before("k_remod");
+        k_remod<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(total, out, albedo, direct);
+    }
+    return finish(ctx, trace);
+}
+
+flr_status flr_denoise_modulated(int32_t n, int32_t Q, int32_t W, int32_t H, const float* guides,
+                                 const float* radiance_mod, const float* albedo, const float* direct,
+                                 float albedo_floor, const flr_params* p, float* out, void* workspace,
+                                 size_t workspace_bytes, flr_stream_t stream)
+{
+    return flr_denoise_modulated_traced(n, Q, W, H, guides, radiance_mod, albedo, direct, albedo_floor, p, out,
+                                        workspace, workspace_bytes, stream, nullptr);
 }
 
 flr_status flr_denoise(int32_t n, int32_t Q, int32_t W, int32_t H, const float* guides,

@@ -18,10 +18,11 @@ constexpr int kApplyWsNC = 7;  // consumer warps (+1 producer = 8 warps, 255-reg
 constexpr int kApplyWsS = 4;   // guide-row stages per consumer
 constexpr int kApplyWsM = 2;   // model stages per consumer
 
-template <int Q>
+template <int Q, bool MOD = false>
 struct ApplyWsCfg {
     using SD = StreamDims<Q>;
-    static constexpr int ROWF = Q * kSeg;                 // floats per guide-row stage
+    // floats per row stage: Q guide planes (+ 3 albedo and 3 direct-light planes)
+    static constexpr int ROWF = (Q + (MOD ? 6 : 0)) * kSeg;
     static constexpr int MODF = 2 * kApplyNCol * SD::MS;  // floats per model stage
     // as many guide-row stages (<= kApplyWsS) as fit in 227 KB with 7 consumers
     static constexpr int fit_stages(int s)
@@ -35,13 +36,16 @@ struct ApplyWsCfg {
     static constexpr int NBAR = 2 * (S + SM);  // full + empty per stage
     static constexpr size_t SMEM = BAR_OFF + (size_t)NC * NBAR * sizeof(uint64_t);
     static_assert(WARPF % 32 == 0 && ROWF % 32 == 0 && MODF % 4 == 0, "16-byte aligned stages");
-    static_assert(SMEM <= 232448, "apply pipeline exceeds 227 KB of shared memory");
+    // the modulated variant (6 more planes per row) does not fit for the largest Q: those
+    // shapes remodulate in a separate elementwise kernel (apply_mod_supported)
+    static constexpr bool FITS = SMEM <= 232448;
+    static_assert(FITS || MOD, "apply pipeline exceeds 227 KB of shared memory");
 };
 
-template <int Q>
-__global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __grid_constant__ ApplyArgs a, int n)
+template <int Q, bool MOD = false>
+__global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(const __grid_constant__ ApplyArgs a, int n)
 {
-    using C = ApplyWsCfg<Q>;
+    using C = ApplyWsCfg<Q, MOD>;
     using SD = StreamDims<Q>;
     constexpr int NC = C::NC, S = C::S, SM = C::SM, MS = SD::MS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -61,7 +65,8 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __
 
     auto geom = [&](int it, int& f) {
         f = it / per_frame;
-        const int rem = it - f * per_frame;
+        int rem = it - f * per_frame;
+        if (a.reverse) rem = per_frame - 1 - rem;
         return apply_geom(a, rem / a.nseg, rem - (rem / a.nseg) * a.nseg);
     };
 
@@ -93,7 +98,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __
             int pit = it, py0 = y;
             for (; kr < S && pit < nitems && py0 < g.y1; ++kr, ++py0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                apply_issue_row<Q>(a, g, f, py0, rows_st + kr * C::ROWF, &rfull[kr], pg);
+                apply_issue_row<Q, MOD>(a, g, f, py0, rows_st + kr * C::ROWF, &rfull[kr], pg);
             }
             pre = kr;
         }
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __
                 const int s = kr % S;
                 if (kr < S || mbar_test_wait(&rempty[s], ((kr / S) - 1) & 1)) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    apply_issue_row<Q>(a, g, f, y, rows_st + s * C::ROWF, &rfull[s], pg);
+                    apply_issue_row<Q, MOD>(a, g, f, y, rows_st + s * C::ROWF, &rfull[s], pg);
                     ++kr;
                     if (++y == g.y1) {
                         it += GW;
@@ -217,6 +222,18 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q>::THREADS, 1) k_apply_ws(const __
                         p1 = fma2(gp[j], bc2(m1[(1 + j) * 3 + cc]), p1);
                     }
                     upk2(fma2(t2[h], sub2(p1, p0), p0), o[cc][2 * h], o[cc][2 * h + 1]);
+                }
+            }
+            if (MOD) {  // remodulation and direct light: out = albedo * I + direct (R21)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    const float4 al = reinterpret_cast<const float4*>(st + (Q + cc) * kSeg)[lane];
+                    float4 dl = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (a.has_direct) dl = reinterpret_cast<const float4*>(st + (Q + 3 + cc) * kSeg)[lane];
+                    o[cc][0] = fmaf(al.x, o[cc][0], dl.x);
+                    o[cc][1] = fmaf(al.y, o[cc][1], dl.y);
+                    o[cc][2] = fmaf(al.z, o[cc][2], dl.z);
+                    o[cc][3] = fmaf(al.w, o[cc][3], dl.w);
                 }
             }
             __syncwarp();  // guide stage consumed by every lane

@@ -23,9 +23,10 @@ constexpr int kFitWsNC = 7;  // consumer warps (+1 producer = 8 warps: 2 per SMS
 #endif
 constexpr int kFitWsS = FLR_FITWS_S;  // ring stages per consumer
 
-template <int Q>
+template <int Q, bool MOD = false>
 struct FitWsCfg {
-    static constexpr int STG = StreamDims<Q>::STG_FIT;  // floats per stage (one pixel row)
+    // floats per stage (one pixel row): Q guide planes, 3 radiance planes (+ 3 albedo planes)
+    static constexpr int STG = StreamDims<Q>::STG_FIT + (MOD ? 3 * kSeg : 0);
     // as many stages (<= kFitWsS) as fit in 227 KB with 7 consumers
     static constexpr int fit_stages(int s)
     {
@@ -83,11 +84,12 @@ __device__ __forceinline__ void fold_pairs(const f2 (&in)[N], float (&out)[N], i
 }
 
 // the rows of one item for one consumer warp (k: rows consumed so far by this warp)
-template <int Q, int D, bool EDGE>
+template <int Q, int D, bool EDGE, bool MOD>
 __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], const float* ring, uint64_t* full,
-                                            uint64_t* empty, int& k, int rows, int lane, int lb0, int x0, int W)
+                                            uint64_t* empty, int& k, int rows, int lane, int lb0, int x0, int W,
+                                            float afloor)
 {
-    constexpr int S = FitWsCfg<Q>::S, STG = FitWsCfg<Q>::STG;
+    constexpr int S = FitWsCfg<Q, MOD>::S, STG = FitWsCfg<Q, MOD>::STG;
     {  // the block shift c = its top-left pixel (first row of the item)
         mbar_wait(&full[k % S], (k / S) & 1);
         const float* st = ring + (k % S) * STG;
@@ -106,6 +108,14 @@ __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], c
             for (int j = 0; j < Q; ++j) d[j] = reinterpret_cast<const f2*>(st + j * kSeg)[2 * lane + h];
 #pragma unroll
             for (int c = 0; c < 3; ++c) y[c] = reinterpret_cast<const f2*>(st + (Q + c) * kSeg)[2 * lane + h];
+            if (MOD) {  // demodulation y = radiance / max(albedo, floor) (R20)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const f2 al = reinterpret_cast<const f2*>(st + (Q + 3 + c) * kSeg)[2 * lane + h];
+                    y[c] = pk2(lo2(y[c]) * __frcp_rn(fmaxf(lo2(al), afloor)),
+                               hi2(y[c]) * __frcp_rn(fmaxf(hi2(al), afloor)));
+                }
+            }
 #pragma unroll
             for (int j = 0; j < Q; ++j) d[j] = sub2(d[j], bc2(cs[j]));
             if (EDGE) {  // pixels past the image arrive as zeros: make them contribute nothing
@@ -120,10 +130,10 @@ __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], c
     }
 }
 
-template <int Q, int D>
-__global__ void __launch_bounds__(FitWsCfg<Q>::THREADS, 1) k_fit_ws(const __grid_constant__ FitArgs a, int n)
+template <int Q, int D, bool MOD = false>
+__global__ void __launch_bounds__(FitWsCfg<Q, MOD>::THREADS, 1) k_fit_ws(const __grid_constant__ FitArgs a, int n)
 {
-    using C = FitWsCfg<Q>;
+    using C = FitWsCfg<Q, MOD>;
     using Dm = Dims<Q>;
     constexpr int NC = C::NC, S = C::S, STG = C::STG, DQ = D / 4;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -147,7 +157,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q>::THREADS, 1) k_fit_ws(const __grid
         // ---------------- producer: lane c feeds consumer c ----------------
         if (lane >= NC) return;
         const int c = lane;
-        const uint64_t pg = std_policy_guides_fit(), py = policy_evict_first();
+        const uint64_t pg = policy_by_code(a.gpol), py = policy_evict_first();
         int it = blockIdx.x * NC + c, row = 0, rows = 0, f = 0, by = 0, sg = 0;
         auto decode = [&]() {
             if (it >= nitems) return;
@@ -166,7 +176,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q>::THREADS, 1) k_fit_ws(const __grid
             const int slot = k % S;
             if (it < nitems && (k < S || mbar_test_wait(&empty[c * S + slot], ((k / S) - 1) & 1))) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                fit_issue_row<Q, D>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
+                fit_issue_row<Q, D, MOD>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
                                     pg, py);
                 ++k;
                 if (++row == rows) {
@@ -191,9 +201,11 @@ __global__ void __launch_bounds__(FitWsCfg<Q>::THREADS, 1) k_fit_ws(const __grid
         FitAccPix<Q> acc;
         acc.zero();
         if (sg * kSeg + kSeg > a.W)  // segment reaches past the image
-            fit_ws_rows<Q, D, true>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W);
+            fit_ws_rows<Q, D, true, MOD>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
+                                         a.afloor);
         else
-            fit_ws_rows<Q, D, false>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W);
+            fit_ws_rows<Q, D, false, MOD>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
+                                          a.afloor);
         // epilogue: fold, then un-shift to fp64 and store (lanes of a block split the components)
         float u[Q], sv[Dm::NS], yc[3], xy[3 * Q];
         fold_pairs(acc.U, u, DQ);

@@ -22,12 +22,13 @@ namespace flr {
 // dev build: this Q is compiled out (see build.py FLR_QS); calls report FLR_ERR_UNSUPPORTED
 template <int Q>
 void launch_fit(int, int, int, int, int, int, const float*, const float*, float*, double*, double*, float*,
-                int, double, double, const Taps&, LaunchCtx& ctx)
+                int, double, double, const Taps&, LaunchCtx& ctx, const float*, float)
 {
     ctx.unsupported = true;
 }
 template <int Q>
-void launch_apply(int, int, int, int, int, int, const float*, int, const float*, float*, LaunchCtx& ctx)
+void launch_apply(int, int, int, int, int, int, const float*, int, const float*, float*, LaunchCtx& ctx,
+                  const float*, const float*)
 {
     ctx.unsupported = true;
 }
@@ -73,8 +74,24 @@ static int num_sms()
 // returns true when the TMA-ring kernel ran with `done` row counters (K2 may then wait per row)
 template <int Q, int D>
 static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
-                      int* done, cudaStream_t s)
+                      int* done, cudaStream_t s, const float* A, float afloor)
 {
+    if (A) {  // modulated fit: the warp-specialised kernel with the albedo planes in its ring
+        FitArgs a;
+        if (!make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kSeg, 3) ||
+            !make_tmap_planes(&a.ta, A, W, H, n * 3, kSeg, 3))
+            return false;
+        a.mom = mom;
+        a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
+        a.done = nullptr;
+        a.gpol = 0;
+        a.afloor = afloor;
+        using C = FitWsCfg<Q, true>;
+        const int grid = min(num_sms(), cdiv(n * By * a.nseg, C::NC));
+        set_smem(k_fit_ws<Q, D, true>, C::SMEM);
+        launch_pdl(k_fit_ws<Q, D, true>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+        return false;
+    }
     static const bool use_ldg = std::getenv("FLR_FIT_LDG") != nullptr;
     if (use_ldg && vec_ok(G, W) && vec_ok(Y, W)) {  // LDG-prefetch persistent kernel (memory-latency bound)
         FitLdgArgs la{G, Y, mom, W, H, Bx, mom_pitch(Bx), By, cdiv(W, kSeg)};
@@ -89,6 +106,9 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
         a.mom = mom;
         a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
         a.done = done;
+        static const int gpol = std::getenv("FLR_FIT_GPOL") ? std::atoi(std::getenv("FLR_FIT_GPOL")) : 0;
+        a.gpol = gpol;
+
         const int items = n * By * a.nseg;
         static const bool ring = std::getenv("FLR_FIT_RING") != nullptr;
         if (ring) {  // per-warp self-feeding rings (lane 0 of each warp issues its own TMA)
@@ -120,7 +140,7 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
 template <int Q>
 void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, const float* Y,
                 float* raw, double* mom, double* hb, float* models, int mstride, double ea,
-                double em, const Taps& taps, LaunchCtx& ctx)
+                double em, const Taps& taps, LaunchCtx& ctx, const float* A, float afloor)
 {
     const cudaStream_t s = ctx.s;
     // wavefront flags: fit_done [n][By] | k2_done [n][ceil(By / kK2TY)]
@@ -131,10 +151,10 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     bool fit_signals = false;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
-        ctx.before(!vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : std::getenv("FLR_FIT_RING") ? "k_fit_stream" : "k_fit_ws");
-        if (D == 4) fit_signals = launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, fit_done, s);
-        else if (D == 8) fit_signals = launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, fit_done, s);
-        else fit_signals = launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, fit_done, s);
+        ctx.before(A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : std::getenv("FLR_FIT_RING") ? "k_fit_stream" : "k_fit_ws");
+        if (D == 4) fit_signals = launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor);
+        else if (D == 8) fit_signals = launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor);
+        else fit_signals = launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor);
     } else {
         ctx.before("k_moments_small");
         k_moments_small<Q><<<dim3(cdiv(Bx, 128), By, n), 128, 0, s>>>(W, H, Bx, By, D, G, Y, raw);
@@ -159,6 +179,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
         // default: one tile kernel, moment field read once (+ halo) by TMA, no blurred-field
         // round trip through L2
         const dim3 grid(cdiv(Bx, kK2TX), cdiv(By, kK2TY), n);
+        static const int k2pol = std::getenv("FLR_K2_POL") ? std::atoi(std::getenv("FLR_K2_POL")) : 1;
 #define FLR_KT(RR)                                                                                          \
     case RR: {                                                                                              \
         using KG = K2Geom<Q, RR>;                                                                           \
@@ -168,7 +189,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
         ctx.before("k_blur_solve_tile");                                                                    \
         set_smem(k_blur_solve_tile<Q, RR>, KG::SMEM);                                                       \
         launch_pdl(k_blur_solve_tile<Q, RR>, grid, dim3(kK2Threads), KG::SMEM, s, tm, Bx, By, models, ea, em, \
-                   taps, (const int*)(fit_signals ? fit_done : nullptr), cdiv(W, kSeg), k2_done);           \
+                   taps, (const int*)(fit_signals ? fit_done : nullptr), cdiv(W, kSeg), k2_done, k2pol);    \
         k2tile = true;                                                                                      \
         break;                                                                                              \
     }
@@ -226,9 +247,38 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
 
 template <int Q>
 void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* models, int mstride,
-                  const float* G, float* out, LaunchCtx& ctx)
+                  const float* G, float* out, LaunchCtx& ctx, const float* A, const float* Dl)
 {
     const cudaStream_t s = ctx.s;
+    if constexpr (!ApplyWsCfg<Q, true>::FITS) {
+        if (A) {
+            ctx.unsupported = true;
+            return;
+        }
+    } else if (A) {  // modulated apply (caller checked apply_mod_fused): warp-specialised kernel only
+        ApplyArgs a;
+        std::memset(&a, 0, sizeof(a));
+        if (mstride != Dims<Q>::MSTRIDE || !make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q) ||
+            !make_tmap_planes(&a.ta, A, W, H, n * 3, kSeg, 3) ||
+            (Dl && !make_tmap_planes(&a.td, Dl, W, H, n * 3, kSeg, 3))) {
+            ctx.unsupported = true;
+            return;
+        }
+        a.has_direct = Dl != nullptr;
+        a.models = models, a.out = out;
+        a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W, kSeg), a.nband = apply_nband(H, D, By);
+        a.nsub = 1;
+        while (D % (2 * a.nsub) == 0 && D / (2 * a.nsub) >= 4)
+            a.nsub *= 2;
+        a.reverse = 1;
+        using C = ApplyWsCfg<Q, true>;
+        const int items = n * a.nseg * a.nband * a.nsub;
+        const int grid = min(num_sms(), cdiv(items, C::NC));
+        ctx.before("k_apply_ws_mod");
+        set_smem(k_apply_ws<Q, true>, C::SMEM);
+        launch_pdl(k_apply_ws<Q, true>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+        return;
+    }
     if (D % 8 == 0 && mstride == Dims<Q>::MSTRIDE && aligned(models, 16)) {
         const int off = (D / 2) % 8;
         ApplyArgs a;
@@ -243,6 +293,8 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
                 a.nsub *= 2;
             if (const char* e = std::getenv("FLR_APPLY_NSUB")) a.nsub = std::max(1, std::atoi(e));
             if (D % a.nsub) a.nsub = 1;
+            static const int rev = std::getenv("FLR_APPLY_REV") ? std::atoi(std::getenv("FLR_APPLY_REV")) : 1;
+            a.reverse = rev;
             a.ready = ctx.wave_k2, a.ready_target = ctx.wave_target, a.nrt = ctx.wave_nrt, a.ready_ty = kK2TY;
             ctx.wave_k2 = nullptr;
             const int items = n * a.nseg * a.nband * a.nsub;
@@ -345,9 +397,19 @@ bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx)
 
 template void launch_fit<FLR_Q>(int, int, int, int, int, int, const float*, const float*, float*,
                                 double*, double*, float*, int, double, double, const Taps&,
-                                LaunchCtx&);
+                                LaunchCtx&, const float*, float);
 template void launch_apply<FLR_Q>(int, int, int, int, int, int, const float*, int, const float*,
-                                  float*, LaunchCtx&);
+                                  float*, LaunchCtx&, const float*, const float*);
 template bool launch_fused<FLR_Q>(const FusedLaunch&, LaunchCtx&);
+template <int Q>
+bool apply_mod_supported()
+{
+#ifdef FLR_STUB
+    return false;
+#else
+    return ApplyWsCfg<Q, true>::FITS;
+#endif
+}
+template bool apply_mod_supported<FLR_Q>();
 
 }  // namespace flr

@@ -61,7 +61,7 @@ template <int Q, int R>
 __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
     k_blur_solve_tile(const __grid_constant__ CUtensorMap tm, int Bx, int By, float* __restrict__ models,
                       double eps_add, double eps_mul, const __grid_constant__ Taps t, const int* wait_rows,
-                      int wait_target, int* signal)
+                      int wait_target, int* signal, int kpol)
 {
     using Dm = Dims<Q>;
     using KG = K2Geom<Q, R>;
@@ -74,11 +74,16 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
     uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(smk) + KG::BAR_OFF);
     const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
     const int bx0 = blockIdx.x * TX, by0 = blockIdx.y * TY, f = blockIdx.z;
+#ifdef FLR_DBG_PHASES
+    extern __device__ long long g_flr_phase[];
+    const int cta_id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (tid == 0) g_flr_phase[1000 + 4 * cta_id] = gtimer();
+#endif
     auto issue = [&](int grp) {
         uint64_t* b = &bar[grp % S];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage before
         mbar_arrive_expect_tx(b, KG::BOXD * sizeof(double));
-        tma_load_3d(ring + (grp % S) * KG::BOX, &tm, bx0 - RE, by0 - R, f * KM + grp * G, b, policy_evict_normal());
+        tma_load_3d(ring + (grp % S) * KG::BOX, &tm, bx0 - RE, by0 - R, f * KM + grp * G, b, policy_by_code(kpol));
     };
     if (tid == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&bar[i], 1);
@@ -194,6 +199,10 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
         const float* src = mstage + r * TX * MS;
         for (int i = tid; i < nbx * MS; i += kK2Threads) dst[i] = src[i];
     }
+#ifdef FLR_DBG_PHASES
+    __syncthreads();
+    if (tid == 0) g_flr_phase[1000 + 4 * cta_id + 1] = gtimer(), g_flr_phase[1000 + 4 * cta_id + 2] = tsg[NG + 2] - tsg[0];
+#endif
     if (signal) {  // publish this tile's models to the APPLY wavefront
         __syncthreads();
         if (tid == 0) red_release_add(&signal[f * gridDim.y + blockIdx.y], 1);

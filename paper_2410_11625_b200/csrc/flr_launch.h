@@ -82,15 +82,34 @@ struct LaunchCtx {
 };
 
 // K1 -> K2a -> K2b -> K3 into `models` (mstride floats per block)
+// A (optional): albedo [n][3][H][W]; the fit then uses Y / max(A, afloor) as its radiance
+// (demodulation fused into the moment kernel; only when fit_mod_fused() holds)
 template <int Q>
 void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, const float* Y,
                 float* raw, double* mom, double* hb, float* models, int mstride, double ea,
-                double em, const Taps& taps, LaunchCtx& ctx);
+                double em, const Taps& taps, LaunchCtx& ctx, const float* A = nullptr, float afloor = 0.f);
 
 // K4 with the fastest kernel the shape allows
+// A (optional): albedo [n][3][H][W]; out = A * I + Dl (Dl optional direct light), fused into
+// the apply kernel's stores (only when apply_mod_fused() holds)
 template <int Q>
 void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* models, int mstride,
-                  const float* G, float* out, LaunchCtx& ctx);
+                  const float* G, float* out, LaunchCtx& ctx, const float* A = nullptr,
+                  const float* Dl = nullptr);
+
+// shapes for which the modulated (albedo) protocol runs fused into the TMA kernels
+inline bool fit_mod_fused(int D, int W, const void* G, const void* Y, const void* A)
+{
+    return (D == 4 || D == 8 || D == 16) && vec_ok(G, W) && vec_ok(Y, W) && vec_ok(A, W);
+}
+template <int Q>
+bool apply_mod_supported();  // the fused modulated apply kernel fits in shared memory for this Q
+inline bool apply_mod_fused(int D, int W, const void* models, const void* G, const void* out, const void* A,
+                            const void* Dl)
+{
+    return D % 8 == 0 && aligned(models, 16) && vec_ok(G, W) && vec_ok(out, W) && vec_ok(A, W) &&
+           (!Dl || vec_ok(Dl, W));
+}
 
 // the fused single-kernel schedule (flr_fused.cuh); returns false when this (Q, D_fit,
 // D_out, R, alignment) combination is not compiled in, so the caller falls back to the
@@ -111,10 +130,12 @@ bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx);
 #define FLR_DECLARE_Q(Q)                                                                          \
     extern template void launch_fit<Q>(int, int, int, int, int, int, const float*, const float*,  \
                                        float*, double*, double*, float*, int, double, double,     \
-                                       const Taps&, LaunchCtx&);                          \
+                                       const Taps&, LaunchCtx&, const float*, float);             \
     extern template void launch_apply<Q>(int, int, int, int, int, int, const float*, int,         \
-                                         const float*, float*, LaunchCtx&);                     \
-    extern template bool launch_fused<Q>(const FusedLaunch&, LaunchCtx&);
+                                         const float*, float*, LaunchCtx&, const float*,          \
+                                         const float*);                                           \
+    extern template bool launch_fused<Q>(const FusedLaunch&, LaunchCtx&);                      \
+    extern template bool apply_mod_supported<Q>();
 FLR_DECLARE_Q(1) FLR_DECLARE_Q(2) FLR_DECLARE_Q(3) FLR_DECLARE_Q(4) FLR_DECLARE_Q(5)
 FLR_DECLARE_Q(6) FLR_DECLARE_Q(7) FLR_DECLARE_Q(8) FLR_DECLARE_Q(9) FLR_DECLARE_Q(10)
 FLR_DECLARE_Q(11) FLR_DECLARE_Q(12) FLR_DECLARE_Q(13) FLR_DECLARE_Q(14) FLR_DECLARE_Q(15)

@@ -56,6 +56,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity)
     }
 }
 
+__device__ __forceinline__ long long gtimer()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---- L2 cache policies --------------------------------------------------------
 __device__ __forceinline__ uint64_t policy_evict_first()
 {
@@ -74,6 +81,29 @@ __device__ __forceinline__ uint64_t policy_evict_normal()
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last_frac(float f)
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(f));
+    return p;
+}
+// policy codes (kernel arguments): 0 evict_first, 1 evict_normal, 2 evict_last,
+// 3 / 4 evict_last for 3/4 / 1/2 of the lines (the rest evict_first)
+__device__ __forceinline__ uint64_t policy_by_code(int code)
+{
+    switch (code) {
+    case 1: return policy_evict_normal();
+    case 2: return policy_evict_last();
+    case 3: return policy_evict_last_frac(0.75f);
+    case 4: return policy_evict_last_frac(0.5f);
+    default: return policy_evict_first();
+    }
+}
+// fp64 store with an L2 cache-policy hint
+__device__ __forceinline__ void st_hint_f64(double* p, double v, uint64_t pol)
+{
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
 // ---- bulk copy global -> shared (bytes % 16 == 0, both addresses 16-byte aligned) ----

@@ -105,16 +105,20 @@ struct FitArgs {
     double* mom;     // [n][KM][By][Bxp]
     int W, H, Bx, Bxp, By, nseg;
     int* done;       // optional [n][By] row counters (+1 per finished item, release)
+    int gpol;        // L2 policy code (policy_by_code) of the guide reads
+    CUtensorMap ta;  // albedo [n*3][H][W], box {128, 1, 3} (modulated fit only)
+    float afloor;    // albedo floor of the demodulation (modulated fit only)
 };
 
-template <int Q, int D>
+template <int Q, int D, bool MOD = false>
 __device__ __forceinline__ void fit_issue_row(const FitArgs& a, int f, int by, int sg, int rr, float* dst,
                                               uint64_t* bar, uint64_t pol_g, uint64_t pol_y)
 {
-    mbar_arrive_expect_tx(bar, (Q + 3) * kSeg * 4);
+    mbar_arrive_expect_tx(bar, (Q + 3 + (MOD ? 3 : 0)) * kSeg * 4);
     const int x = sg * kSeg, y = by * D + rr;
     tma_load_3d(dst, &a.tg, x, y, f * Q, bar, pol_g);
     tma_load_3d(dst + Q * kSeg, &a.ty, x, y, f * 3, bar, pol_y);
+    if (MOD) tma_load_3d(dst + (Q + 3) * kSeg, &a.ta, x, y, f * 3, bar, pol_y);
 }
 
 // packed-pair layout of the FIT accumulators: d is paired over planes (2p, 2p+1)
@@ -398,6 +402,9 @@ struct ApplyArgs {
     int nsub;  // sub-bands per band (D % nsub == 0): more, smaller APPLY items for one frame
     const int* ready;  // optional [n][nrt] K2 tile-row counters (complete at ready_target)
     int ready_target, nrt, ready_ty;  // ready_ty: block rows per counter
+    int reverse;  // walk each frame's items bottom-up (the rows the fit read last come first)
+    CUtensorMap ta, td;  // albedo, direct [n*3][H][W], box {128, 1, 3} (modulated apply only)
+    int has_direct;      // modulated apply: 0 = no direct-light planes (treated as zero)
 };
 
 __host__ __device__ inline int apply_nband(int H, int D, int By)
@@ -445,12 +452,16 @@ __device__ __forceinline__ void apply_issue_models(const ApplyArgs& a, const App
 }
 
 // guide row y of an APPLY item (lane 0)
-template <int Q>
+template <int Q, bool MOD = false>
 __device__ __forceinline__ void apply_issue_row(const ApplyArgs& a, const ApplyGeom& g, int f, int y, float* dst,
                                                 uint64_t* bar, uint64_t pol_g)
 {
-    mbar_arrive_expect_tx(bar, Q * kSeg * 4);
+    mbar_arrive_expect_tx(bar, (Q + (MOD ? (a.has_direct ? 6 : 3) : 0)) * kSeg * 4);
     tma_load_3d(dst, &a.tg, g.xs, y, f * Q, bar, pol_g);
+    if (MOD) {  // remodulation planes: albedo, then the direct light
+        tma_load_3d(dst + Q * kSeg, &a.ta, g.xs, y, f * 3, bar, pol_g);
+        if (a.has_direct) tma_load_3d(dst + (Q + 3) * kSeg, &a.td, g.xs, y, f * 3, bar, pol_g);
+    }
 }
 
 // stream warp.  `mod` = per-warp [2][kApplyNCol][MS] raw models, `lerp` = [kApplyNCol][MS].

@@ -282,6 +282,26 @@ def frame(W: int, H: int, Q: int = 8, seed: int = 1000, device="cpu", noise: boo
     return G, Y
 
 
+def modulated_frame(W: int, H: int, Q: int = 8, seed: int = 1000, device="cpu"):
+    """Inputs of the paper's albedo protocol, as a renderer would
+    hand them over: (guides [Q,H,W], radiance_mod [3,H,W] = albedo x noisy indirect light,
+    albedo [3,H,W] RGB in [0, 0.95], direct [3,H,W] noise-free direct light >= 0).
+    No FLR arithmetic here: the modulation is the renderer's product A * L."""
+    scene = Scene(seed)
+    R = _render(scene, W, H, device)
+    G = _planes(scene, R, list(guide_names(Q)))
+    Y = _radiance(scene, R, W, H, seed, True, device)
+    dev = torch.device(device)
+    f32 = torch.float32
+    alb = R["alb"].to(f32)
+    tint = torch.stack([_uniform(seed, 20 + c, R["kind"].to(torch.int64), dev) for c in range(3)])
+    A = (alb[None] * (0.7 + 0.3 * tint)).clamp(0.0, 0.95)
+    light = torch.tensor(scene.light, dtype=f32, device=dev)
+    lam = (R["nrm"] * light).sum(-1).clamp_min(0.0)
+    Dl = torch.stack([2.0 * lam * R["ao"] * float(scene.tint[c]) for c in range(3)])
+    return G, (A * Y).to(f32).contiguous(), A.to(f32).contiguous(), Dl.to(f32).contiguous()
+
+
 def batch(n: int, W: int, H: int, Q: int = 8, seed0: int = 1000, device="cpu", **kw):
     """n frames with seeds seed0 .. seed0+n-1: (guides [n,Q,H,W], radiance [n,3,H,W])."""
     gs, ys = zip(*(frame(W, H, Q, seed0 + i, device, **kw) for i in range(n)))

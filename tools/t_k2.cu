@@ -61,7 +61,7 @@ int main(int argc, char** argv)
         float tt = 0;
         for (int rep = 0; rep < 2000; ++rep) {
             if (rep == 1990) cudaEventRecord(e[0]);
-            k_blur_solve_tile<Q, R><<<gt, kK2Threads, KG::SMEM>>>(tmk, Bx, By, models, 1e-5, 1e-4, t, nullptr, 0, nullptr);
+            k_blur_solve_tile<Q, R><<<gt, kK2Threads, KG::SMEM>>>(tmk, Bx, By, models, 1e-5, 1e-4, t, nullptr, 0, nullptr, 1);
         }
         cudaEventRecord(e[1]);
         cudaEventSynchronize(e[1]);
@@ -74,6 +74,20 @@ int main(int argc, char** argv)
         printf("  tile phases (cycles):");
         for (int i = 0; i < ph[63]; ++i) printf(" %lld", ph[i]);
         printf("\n");
+        {
+            const int nc = gt.x * gt.y * gt.z;
+            std::vector<long long> g(1000 + 4 * nc);
+            cudaMemcpyFromSymbol(g.data(), g_flr_phase, g.size() * 8);
+            long long e0 = g[1000], e1 = g[1000], x0 = g[1001], x1 = g[1001];
+            double cyc = 0;
+            for (int c = 0; c < nc; ++c) {
+                e0 = std::min(e0, g[1000 + 4 * c]), e1 = std::max(e1, g[1000 + 4 * c]);
+                x0 = std::min(x0, g[1001 + 4 * c]), x1 = std::max(x1, g[1001 + 4 * c]);
+                cyc += g[1002 + 4 * c];
+            }
+            printf("  CTA entry spread %.2f us, exits %.2f..%.2f us after first entry, mean in-CTA cycles %.0f\n",
+                   (e1 - e0) * 1e-3, (x0 - e0) * 1e-3, (x1 - e0) * 1e-3, cyc / nc);
+        }
 #endif
     }
     printf("n=%d blur_rows %.2f us/frame  solve_rows %.2f us/frame (%s)\n", n, 1e3 * tb / n, 1e3 * tsv / n,
