@@ -47,10 +47,12 @@ def lib():
         L.flr_ref_denoise.argtypes = [i, i, i, i, i, d, i, d, d, fp, fp, dp]
         L.flr_ref_denoise_upsample.argtypes = [i, i, i, i, i, i, d, i, d, d, fp, fp, fp, dp]
         L.flr_ref_denoise_modulated.argtypes = [i, i, i, i, i, d, i, d, d, d, fp, fp, fp, fp, dp]
+        L.flr_ref_solve_block_tikhonov.argtypes = [i, dp, dp, d, dp]
+        L.flr_ref_fit_tikhonov.argtypes = [i, i, i, i, i, i, d, i, d, fp, fp, dp]
         L.flr_ref_num_threads.argtypes = []
         for name in ("flr_ref_moments", "flr_ref_gauss_taps", "flr_ref_blur", "flr_ref_solve_block",
                      "flr_ref_fit", "flr_ref_apply", "flr_ref_denoise", "flr_ref_denoise_upsample",
-                     "flr_ref_num_threads"):
+                     "flr_ref_num_threads", "flr_ref_solve_block_tikhonov", "flr_ref_fit_tikhonov"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -155,6 +157,36 @@ def fit(guides, radiance, D=8, sigma=10.0, R=None, eps_add=1e-5, eps_mul=1e-4, U
     _check(lib().flr_ref_fit(n, Q, W, H, D, U, float(sigma), int(R), float(eps_add),
                              float(eps_mul), gp, rp, Ap), "flr_ref_fit")
     return A
+
+
+def solve_block_tikhonov(M, N, eps=1e-6):
+    M, Mp = _f64(M)
+    N, Np = _f64(N)
+    P = M.shape[0]
+    A, Ap = _out((P, 3))
+    _check(lib().flr_ref_solve_block_tikhonov(P, Mp, Np, float(eps), Ap), "flr_ref_solve_block_tikhonov")
+    return A
+
+
+def fit_tikhonov(guides, radiance, D=8, sigma=10.0, R=None, eps=1e-6, U=1):
+    """Models of the Tikhonov solver (Eq. tikhonov, Fig. 3; R18, R22)."""
+    g, r = _frames(guides, radiance)
+    n, Q, H, W = g.shape
+    if R is None:
+        R = default_radius(sigma, D * U)
+    Bx, By = blocks(W, H, D)
+    g, gp = _f32(g)
+    r, rp = _f32(r)
+    A, Ap = _out((n, By, Bx, Q + 1, 3))
+    _check(lib().flr_ref_fit_tikhonov(n, Q, W, H, D, U, float(sigma), int(R), float(eps), gp, rp, Ap),
+           "flr_ref_fit_tikhonov")
+    return A
+
+
+def denoise_tikhonov(guides, radiance, D=8, sigma=10.0, R=None, eps=1e-6):
+    """fit_tikhonov + the same blended apply as denoise()."""
+    A = fit_tikhonov(guides, radiance, D=D, sigma=sigma, R=R, eps=eps)
+    return apply(A, guides, D)
 
 
 def apply(models, guides, D_out):

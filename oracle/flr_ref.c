@@ -251,9 +251,43 @@ int flr_ref_solve_block(int P, const double* M, const double* N,
     return 0;
 }
 
+/* ---------------------------------------------------------------------------
+ * Tikhonov solve (Eq. tikhonov; Fig. 3): the Gaussian-blurred
+ * outer products of Fig. 3 are weighted MEANS (torchvision's kernel sums to one), so
+ * with block moments the system is written on Mbar / n and Nbar / n, n = Mbar_00 the
+ * blurred pixel count (R22):
+ *   A = (Mbar / n + eps I)^-1 (Nbar / n)        over the full P x P system:
+ * the ones channel is part of X, so eps also shrinks the bias (R18).
+ * ------------------------------------------------------------------------- */
+int flr_ref_solve_block_tikhonov(int P, const double* M, const double* N, double eps, double* A)
+{
+    if (P < 2 || P > MAXP || !M || !N || !A) return 1;
+    double Cm[MAXP * MAXP], B[MAXP * 3];
+    const double n = M[0];
+    for (int i = 0; i < P; ++i)
+        for (int j = 0; j < P; ++j) Cm[i * P + j] = M[i * P + j] / n + (i == j ? eps : 0.0);
+    for (int i = 0; i < P; ++i)
+        for (int c = 0; c < 3; ++c) B[i * 3 + c] = N[i * 3 + c] / n;
+    if (gauss_solve(P, Cm, B)) return 2;
+    for (int i = 0; i < P * 3; ++i) A[i] = B[i];
+    return 0;
+}
+
+static int fit_impl_mode(int n, int Q, int W, int H, int D_fit, int U, double sigma, int R,
+                         double eps_add, double eps_mul, int tikhonov, const float* guides,
+                         const float* radiance, const double* radiance_d, double* A);
+
 static int fit_impl(int n, int Q, int W, int H, int D_fit, int U, double sigma, int R,
                     double eps_add, double eps_mul, const float* guides, const float* radiance,
                     const double* radiance_d, double* A)
+{
+    return fit_impl_mode(n, Q, W, H, D_fit, U, sigma, R, eps_add, eps_mul, 0, guides, radiance,
+                         radiance_d, A);
+}
+
+static int fit_impl_mode(int n, int Q, int W, int H, int D_fit, int U, double sigma, int R,
+                         double eps_add, double eps_mul, int tikhonov, const float* guides,
+                         const float* radiance, const double* radiance_d, double* A)
 {
     if (n < 1 || Q < 1 || Q > MAXP - 1 || W < 1 || H < 1 || D_fit < 1 || U < 1 ||
         !(sigma > 0.0) || R < 0 || !(eps_add >= 0.0) || !(eps_mul >= 0.0) ||
@@ -275,8 +309,10 @@ static int fit_impl(int n, int Q, int W, int H, int D_fit, int U, double sigma, 
     int bad = 0;
 #pragma omp parallel for schedule(static) reduction(| : bad)
     for (long idx = 0; idx < nblk; ++idx)
-        bad |= flr_ref_solve_block(P, Mb + idx * P * P, Nb + idx * P * 3, eps_add, eps_mul,
-                                   A + idx * P * 3);
+        bad |= tikhonov ? flr_ref_solve_block_tikhonov(P, Mb + idx * P * P, Nb + idx * P * 3, eps_add,
+                                                       A + idx * P * 3)
+                        : flr_ref_solve_block(P, Mb + idx * P * P, Nb + idx * P * 3, eps_add, eps_mul,
+                                              A + idx * P * 3);
     rc = bad ? 2 : 0;
 done:
     free(M);
@@ -292,6 +328,13 @@ int flr_ref_fit(int n, int Q, int W, int H, int D_fit, int U,
 {
     if (!radiance) return 1;
     return fit_impl(n, Q, W, H, D_fit, U, sigma, R, eps_add, eps_mul, guides, radiance, NULL, A);
+}
+
+int flr_ref_fit_tikhonov(int n, int Q, int W, int H, int D_fit, int U, double sigma, int R, double eps,
+                         const float* guides, const float* radiance, double* A)
+{
+    if (!radiance) return 1;
+    return fit_impl_mode(n, Q, W, H, D_fit, U, sigma, R, eps, 0.0, 1, guides, radiance, NULL, A);
 }
 
 /* ---------------------------------------------------------------------------

@@ -88,6 +88,15 @@ int flr_ref_denoise_modulated(int n, int Q, int W, int H, int D, double sigma, i
                               const float* guides, const float* radiance_mod,
                               const float* albedo, const float* direct, double* out);
 
+/* Tikhonov variant of steps 4-5 (Eq. tikhonov, Fig. 3; R18, R22):
+ * A = (M / n + eps I)^-1 (N / n) on the full P x P system, n = M[0][0], by Gaussian
+ * elimination with partial pivoting.  Returns 2 if singular. */
+int flr_ref_solve_block_tikhonov(int P, const double* M, const double* N, double eps, double* A);
+
+/* Steps 1-3 as flr_ref_fit, then the Tikhonov solve per block. */
+int flr_ref_fit_tikhonov(int n, int Q, int W, int H, int D_fit, int U, double sigma, int R, double eps,
+                         const float* guides, const float* radiance, double* A);
+
 /* Number of OpenMP threads the oracle will use (1 when built without OpenMP). */
 int flr_ref_num_threads(void);
 

@@ -412,3 +412,71 @@ def test_oracle_rejects_bad_arguments(oracle_mod):
         oracle_mod.fit(G, Y, D=4, sigma=-1.0, R=1)
     with pytest.raises(ValueError):
         oracle_mod.fit(G, Y, D=4, sigma=1.0, R=1, eps_mul=1.0)
+
+
+# ---------------------------------------------------------------- P14: Tikhonov solver
+# Eq. tikhonov with Fig. 3's semantics: the blurred outer
+# products are Gaussian-weighted MEANS (the torchvision kernel sums to one) and eps I
+# regularises the full (Q+1) system including the ones channel (R18, R22).
+def test_p14_tikhonov_eps0_equals_unregularised_appendix(oracle_mod):
+    """Both solvers reduce to exact weighted least squares when unregularised."""
+    rng = np.random.default_rng(60)
+    G = rand_planes(rng, 3, 20, 24)
+    Y = rand_planes(rng, 3, 20, 24)
+    a = oracle_mod.fit_tikhonov(G, Y, D=4, sigma=6.0, eps=0.0)
+    b = oracle_mod.fit(G, Y, D=4, sigma=6.0, eps_add=0.0, eps_mul=0.0)
+    np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-11)
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-3, 0.05])
+def test_p14_tikhonov_equals_bruteforce_ridge(oracle_mod, eps):
+    """Per block: argmin_A sum_p (w_p / sum w) ||y_p - x~_p A||^2 + eps ||A||_F^2 from raw
+    pixels by np.linalg.lstsq on sqrt-weighted rows stacked on sqrt(eps) I rows."""
+    rng = np.random.default_rng(61)
+    Q, H, W, D, sigma, R = 2, 18, 21, 4, 5.0, 2
+    G = rand_planes(rng, Q, H, W)
+    Y = rand_planes(rng, 3, H, W)
+    A = oracle_mod.fit_tikhonov(G, Y, D=D, sigma=sigma, R=R, eps=eps)[0]
+    s = sigma / D
+    for by, bx in [(0, 0), (2, 3), (4, 5), (1, 2)]:
+        w = brute.block_pixel_weights(W, H, D, bx, by, s, R).reshape(-1)
+        w = w / w.sum()
+        X = np.concatenate([np.ones((1, H * W)), G.reshape(Q, -1).astype(np.float64)]).T
+        Yf = Y.reshape(3, -1).astype(np.float64).T
+        sw = np.sqrt(w)[:, None]
+        lhs = np.concatenate([X * sw, math.sqrt(eps) * np.eye(Q + 1)])
+        rhs = np.concatenate([Yf * sw, np.zeros((Q + 1, 3))])
+        ref = np.linalg.lstsq(lhs, rhs, rcond=None)[0]
+        np.testing.assert_allclose(A[by, bx], ref, rtol=1e-8, atol=1e-10)
+
+
+def test_p14_tikhonov_d1_is_figure3(oracle_mod):
+    """D = 1, sigma = 10, R = 20 (a 41-tap kernel) at interior pixels is Fig. 3's
+    local_regression written out with numpy: normalised separable Gaussian, einsum outer
+    products, np.linalg.solve(XX + eps I, XY), then x~ . A."""
+    rng = np.random.default_rng(62)
+    Q, H, W, eps = 2, 46, 44, 1e-6
+    G = rand_planes(rng, Q, H, W)
+    Y = rand_planes(rng, 3, H, W)
+    out = oracle_mod.denoise_tikhonov(G, Y, D=1, sigma=10.0, R=20, eps=eps)[0]
+    k1 = np.exp(-np.arange(-20, 21) ** 2 / 200.0)
+    k1 /= k1.sum()
+    k2 = np.outer(k1, k1)
+    X = np.concatenate([np.ones((1, H, W)), G.astype(np.float64)])
+    Yd = Y.astype(np.float64)
+    for (y, x) in [(20, 20), (22, 23), (25, 21)]:
+        win = (slice(y - 20, y + 21), slice(x - 20, x + 21))
+        Xw = X[:, win[0], win[1]]
+        XX = np.einsum("ikl,jkl,kl->ij", Xw, Xw, k2)
+        XY = np.einsum("ikl,jkl,kl->ij", Xw, Yd[:, win[0], win[1]], k2)
+        A = np.linalg.solve(XX + eps * np.eye(Q + 1), XY)
+        np.testing.assert_allclose(out[:, y, x], X[:, y, x] @ A, rtol=1e-9, atol=1e-11)
+
+
+def test_p14_tikhonov_huge_eps_shrinks_to_zero(oracle_mod):
+    """eps -> infinity shrinks every coefficient, the bias included (R18): output -> 0,
+    unlike the appendix solver, whose eps -> infinity limit is a Gaussian blur (P8)."""
+    rng = np.random.default_rng(63)
+    G, Y = _scene(rng)
+    out = oracle_mod.denoise_tikhonov(G, Y, D=4, sigma=8.0, R=2, eps=1e9)
+    assert np.abs(out).max() < 1e-7 * np.abs(Y).max() + 1e-12
