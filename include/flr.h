@@ -76,6 +76,14 @@ typedef enum {
                                FLR_ERR_UNSUPPORTED when not compiled for the shape */
 } flr_variant;
 
+/* Per-block solver. */
+typedef enum {
+    FLR_SOLVER_APPENDIX = 0, /* the paper's normalised, regularised solve, eps_add + eps_mul */
+    FLR_SOLVER_TIKHONOV = 1  /* Eq. tikhonov with Fig. 3's semantics:
+                                A = (Mbar/n + eps_add I)^-1 Nbar/n on the full (Q+1) system, the
+                                bias included (R18, R22); eps_mul is ignored */
+} flr_solver;
+
 typedef struct {
     int32_t block;    /* D_fit: block size in FIT pixels, in {1,2,4,8,16}; default 8 */
     int32_t upsample; /* U >= 1: output pixels per fit pixel (1 = plain denoise) */
@@ -84,10 +92,11 @@ typedef struct {
     double sigma;     /* Gaussian window std in OUTPUT pixels, > 0; default 10 */
     double eps_add;   /* additive regulariser epsilon >= 0; default 1e-5 */
     double eps_mul;   /* multiplicative regulariser epsilon^ in [0,1); default 1e-4 */
+    int32_t solver;   /* flr_solver; default FLR_SOLVER_APPENDIX */
 } flr_params;
 
 /* Fill *p with the defaults: block 8, upsample 1, radius 0 (auto), variant AUTO,
- * sigma 10, eps_add 1e-5, eps_mul 1e-4.  No-op on NULL. */
+ * sigma 10, eps_add 1e-5, eps_mul 1e-4, solver APPENDIX.  No-op on NULL. */
 void flr_default_params(flr_params* p);
 
 /* Static human-readable name of a status; never NULL. */

@@ -20,7 +20,7 @@ import os
 
 __all__ = ["FLRError", "Params", "lib", "lib_path", "workspace_size", "effective_radius", "fit",
            "apply", "denoise", "denoise_upsample", "denoise_modulated", "Denoiser", "EventTrace", "last_launch_count", "last_launch_names",
-           "VARIANT_AUTO", "VARIANT_STAGED", "VARIANT_FUSED"]
+           "VARIANT_AUTO", "VARIANT_STAGED", "VARIANT_FUSED", "SOLVER_APPENDIX", "SOLVER_TIKHONOV"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_PKG, "libflr.so")
@@ -29,6 +29,8 @@ _lib = None
 VARIANT_AUTO = 0
 VARIANT_STAGED = 1
 VARIANT_FUSED = 2
+SOLVER_APPENDIX = 0  # the paper's normalised solve
+SOLVER_TIKHONOV = 1  # Eq. tikhonov, Fig. 3 semantics; eps_add is its epsilon
 
 
 class EventTrace(ctypes.Structure):
@@ -56,13 +58,13 @@ class Params(ctypes.Structure):
     """Mirror of flr_params (include/flr.h)."""
     _fields_ = [("block", ctypes.c_int32), ("upsample", ctypes.c_int32), ("radius", ctypes.c_int32),
                 ("variant", ctypes.c_int32), ("sigma", ctypes.c_double), ("eps_add", ctypes.c_double),
-                ("eps_mul", ctypes.c_double)]
+                ("eps_mul", ctypes.c_double), ("solver", ctypes.c_int32)]
 
     @classmethod
     def make(cls, block=8, upsample=1, sigma=10.0, radius=0, eps_add=1e-5, eps_mul=1e-4,
-             variant=VARIANT_AUTO):
+             variant=VARIANT_AUTO, solver=0):
         return cls(int(block), int(upsample), int(radius), int(variant), float(sigma),
-                   float(eps_add), float(eps_mul))
+                   float(eps_add), float(eps_mul), int(solver))
 
 
 def lib_path() -> str:
@@ -188,7 +190,7 @@ def _ptr(t):
 
 
 def fit(guides, radiance, *, block=8, upsample=1, sigma=10.0, radius=0, eps_add=1e-5,
-        eps_mul=1e-4, variant=VARIANT_AUTO, out=None, workspace=None):
+        eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None, workspace=None):
     """Per-block raw-basis models [n, By, Bx, Q+1, 3]."""
     torch = _torch()
     g = _frames(guides, "guides")
@@ -196,7 +198,7 @@ def fit(guides, radiance, *, block=8, upsample=1, sigma=10.0, radius=0, eps_add=
     n, Q, H, W = g.shape
     if tuple(y.shape) != (n, 3, H, W):
         raise ValueError("radiance must be [n,3,H,W] matching guides")
-    p = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant)
+    p = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver)
     Bx, By = math.ceil(W / block), math.ceil(H / block)
     if out is None:
         out = torch.empty((n, By, Bx, Q + 1, 3), dtype=torch.float32, device=g.device)
@@ -229,7 +231,7 @@ def apply(models, guides, block_out, *, out=None):
 
 
 def denoise(guides, radiance, *, block=8, sigma=10.0, radius=0, eps_add=1e-5, eps_mul=1e-4,
-            variant=VARIANT_AUTO, out=None, workspace=None):
+            variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None, workspace=None):
     """FLR denoise: fit + apply with the same guides.  [n,Q,H,W], [n,3,H,W] -> [n,3,H,W]."""
     torch = _torch()
     g = _frames(guides, "guides")
@@ -237,7 +239,7 @@ def denoise(guides, radiance, *, block=8, sigma=10.0, radius=0, eps_add=1e-5, ep
     n, Q, H, W = g.shape
     if tuple(y.shape) != (n, 3, H, W):
         raise ValueError("radiance must be [n,3,H,W] matching guides")
-    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, variant)
+    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, variant, solver)
     if out is None:
         out = torch.empty((n, 3, H, W), dtype=torch.float32, device=g.device)
     ws_bytes = workspace_size(n, Q, W, H, block=block, sigma=sigma, radius=radius, eps_add=eps_add,
@@ -249,7 +251,8 @@ def denoise(guides, radiance, *, block=8, sigma=10.0, radius=0, eps_add=1e-5, ep
 
 
 def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, sigma=10.0, radius=0,
-                     eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO, out=None, workspace=None):
+                     eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None,
+                     workspace=None):
     """Joint denoise + upsample: fit on low-res radiance/guides, apply with hi-res guides."""
     torch = _torch()
     g = _frames(guides_lo, "guides_lo")
@@ -259,7 +262,7 @@ def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, 
     Hh, Wh = int(gh.shape[2]), int(gh.shape[3])
     if tuple(y.shape) != (n, 3, H, W) or gh.shape[0] != n or gh.shape[1] != Q:
         raise ValueError("shape mismatch between guides_lo, radiance_lo and guides_hi")
-    p = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant)
+    p = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver)
     if out is None:
         out = torch.empty((n, 3, Hh, Wh), dtype=torch.float32, device=g.device)
     ws_bytes = workspace_size(n, Q, W, H, block=block, upsample=upsample, sigma=sigma, radius=radius,
@@ -272,7 +275,8 @@ def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, 
 
 
 def denoise_modulated(guides, radiance_mod, albedo, direct=None, *, block=8, sigma=10.0, radius=0,
-                      eps_add=1e-5, eps_mul=1e-4, albedo_floor=1e-3, out=None, workspace=None):
+                      eps_add=1e-5, eps_mul=1e-4, albedo_floor=1e-3, solver=SOLVER_APPENDIX, out=None,
+                      workspace=None):
     """The paper's protocol: demodulate by max(albedo, floor), FLR-denoise,
     remodulate, add the direct light.  All radiance-like tensors are [n,3,H,W]."""
     torch = _torch()
@@ -284,7 +288,7 @@ def denoise_modulated(guides, radiance_mod, albedo, direct=None, *, block=8, sig
     for t, nm in ((r, "radiance_mod"), (a, "albedo")) + (((d, "direct"),) if d is not None else ()):
         if tuple(t.shape) != (n, 3, H, W):
             raise ValueError(f"{nm} must be [n,3,H,W] matching guides")
-    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, VARIANT_AUTO)
+    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, VARIANT_AUTO, solver)
     if out is None:
         out = torch.empty((n, 3, H, W), dtype=torch.float32, device=g.device)
     ws_bytes = workspace_size(n, Q, W, H, block=block, sigma=sigma, radius=radius, eps_add=eps_add,
@@ -303,10 +307,10 @@ class Denoiser:
     Holds the ctypes argument objects so a call is one C-ABI call with no allocation."""
 
     def __init__(self, n, Q, W, H, device="cuda", block=8, upsample=1, sigma=10.0, radius=0,
-                 eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO):
+                 eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX):
         torch = _torch()
         self.n, self.Q, self.W, self.H, self.U = n, Q, W, H, upsample
-        self.params = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant)
+        self.params = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver)
         nbytes = workspace_size(n, Q, W, H, block=block, upsample=upsample, sigma=sigma, radius=radius,
                                 eps_add=eps_add, eps_mul=eps_mul, variant=variant)
         self.workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)

@@ -29,10 +29,15 @@ flr_status check_params(const flr_params* p)
     if (!(p->eps_add >= 0.0) || !std::isfinite(p->eps_add)) return FLR_ERR_INVALID_VALUE;
     if (!(p->eps_mul >= 0.0) || !(p->eps_mul < 1.0)) return FLR_ERR_INVALID_VALUE;
     if (p->radius < 0) return FLR_ERR_INVALID_VALUE;
+    if (p->solver != FLR_SOLVER_APPENDIX && p->solver != FLR_SOLVER_TIKHONOV) return FLR_ERR_INVALID_VALUE;
     if (p->variant != FLR_VARIANT_AUTO && p->variant != FLR_VARIANT_STAGED && p->variant != FLR_VARIANT_FUSED)
         return FLR_ERR_UNSUPPORTED;
     return FLR_OK;
 }
+
+// eps_mul as the kernels take it: a negative value selects the Tikhonov solve
+// (solve_block_tikhonov in flr_solve.cuh); users cannot pass one (check_params)
+inline double solver_eps_mul(const flr_params* p) { return p->solver == FLR_SOLVER_TIKHONOV ? -1.0 : p->eps_mul; }
 
 // R1: default radius ceil(2 sigma / D_out) blocks (Fig. 3's 41-tap kernel at std 10)
 int effective_radius(const flr_params* p)
@@ -155,7 +160,7 @@ flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, co
     ctx.wave_flags = wave ? (int*)(base + L.flags) : nullptr;
     FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, G, Y, (float*)(base + L.raw),
                                       (double*)(base + L.mom), (double*)(base + L.hb), models,
-                                      mstride, p->eps_add, p->eps_mul, taps, ctx)));
+                                      mstride, p->eps_add, solver_eps_mul(p), taps, ctx)));
     return FLR_OK;
 }
 
@@ -204,6 +209,7 @@ void flr_default_params(flr_params* p)
     p->sigma = 10.0;
     p->eps_add = 1e-5;
     p->eps_mul = 1e-4;
+    p->solver = FLR_SOLVER_APPENDIX;
 }
 
 const char* flr_status_string(flr_status s)
@@ -305,7 +311,7 @@ flr_status flr_denoise_upsample_traced(int32_t n, int32_t Q, int32_t W_lo, int32
         F.mom = (double*)((char*)workspace + L.mom);
         F.models = models;
         F.flags = (int*)((char*)workspace + L.flags);
-        F.eps_add = p->eps_add, F.eps_mul = p->eps_mul;
+        F.eps_add = p->eps_add, F.eps_mul = solver_eps_mul(p);
         F.taps = make_taps(p->sigma / ((double)D * p->upsample), effective_radius(p));
         bool done = false;
         FLR_DISPATCH_Q(Q, (done = launch_fused<QQ>(F, ctx)));
@@ -361,7 +367,7 @@ flr_status flr_denoise_modulated_traced(int32_t n, int32_t Q, int32_t W, int32_t
         char* base = (char*)workspace;
         FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, guides, radiance_mod, (float*)(base + L.raw),
                                           (double*)(base + L.mom), (double*)(base + L.hb), models, ms,
-                                          p->eps_add, p->eps_mul, taps, ctx, albedo, albedo_floor)));
+                                          p->eps_add, solver_eps_mul(p), taps, ctx, albedo, albedo_floor)));
     } else {  // demodulate into `out` (same shape), then the plain fit reads it
         ctx.before("k_demod");
         k_demod<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(total, radiance_mod, albedo, albedo_floor, out);

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(con
         {  // guide rows of the first item, ahead of the models (and of the wait)
             int pit = it, py0 = y;
             for (; kr < S && pit < nitems && py0 < g.y1; ++kr, ++py0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                ws_proxy_fence();
                 apply_issue_row<Q, MOD>(a, g, f, py0, rows_st + kr * C::ROWF, &rfull[kr], pg);
             }
             pre = kr;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(con
             if (need_models) {
                 const int s = km % SM;
                 if (km < SM || mbar_test_wait(&mempty[s], ((km / SM) - 1) & 1)) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    ws_proxy_fence();
                     apply_issue_models<Q>(a, g, f, mod_st + s * C::MODF, &mfull[s], pm);
                     ++km;
                     need_models = false;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(con
             } else {
                 const int s = kr % S;
                 if (kr < S || mbar_test_wait(&rempty[s], ((kr / S) - 1) & 1)) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    ws_proxy_fence();
                     apply_issue_row<Q, MOD>(a, g, f, y, rows_st + s * C::ROWF, &rfull[s], pg);
                     ++kr;
                     if (++y == g.y1) {

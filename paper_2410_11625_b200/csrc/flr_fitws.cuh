@@ -123,7 +123,11 @@ __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], c
 #pragma unroll
                 for (int j = 0; j < Q; ++j) d[j] = pk2(in0 ? lo2(d[j]) : 0.f, in1 ? hi2(d[j]) : 0.f);
             }
+#ifndef FLR_FITWS_NOCOMPUTE
             acc.add(d, y);
+#else
+            if (lo2(d[0]) == 12345.f) acc.add(d, y);  // timing experiment: stream without accumulating
+#endif
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);  // values are in registers: free the stage
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD>::THREADS, 1) k_fit_ws(const _
         while (__any_sync(mask, it < nitems)) {
             const int slot = k % S;
             if (it < nitems && (k < S || mbar_test_wait(&empty[c * S + slot], ((k / S) - 1) & 1))) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                ws_proxy_fence();
                 fit_issue_row<Q, D, MOD>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
                                     pg, py);
                 ++k;

@@ -175,7 +175,8 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     bool k2tile = false;
     // the tile kernel keeps all KM blurred components of a block in registers: up to Q = 8
     // (KM = 72); larger Q take the row variant (components in shared memory)
-    if (Q <= 8 && !tile && !rows && R >= 1 && R <= kTileMaxR && mstride == Dims<Q>::MSTRIDE) {
+    if constexpr (Q <= 8) {  // (not instantiated for larger Q: keeps the build time down)
+    if (!tile && !rows && R >= 1 && R <= kTileMaxR && mstride == Dims<Q>::MSTRIDE) {
         // default: one tile kernel, moment field read once (+ halo) by TMA, no blurred-field
         // round trip through L2
         const dim3 grid(cdiv(Bx, kK2TX), cdiv(By, kK2TY), n);
@@ -195,6 +196,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     }
         switch (R) { FLR_KT(1) FLR_KT(2) FLR_KT(3) FLR_KT(4) FLR_KT(5) FLR_KT(6) FLR_KT(7) FLR_KT(8) }
 #undef FLR_KT
+    }
     }
     if (k2tile) {
         if (k2_done) ctx.wave_k2 = k2_done, ctx.wave_nrt = cdiv(By, kK2TY), ctx.wave_target = cdiv(Bx, kK2TX);
@@ -220,7 +222,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
             launch_pdl(k_solve<Q>, dim3(cdiv(Bx, 128), By, n), dim3(128), 0, s, Bx, Bxp, By, (const double*)hb,
                        models, mstride, ea, em);
         }
-    } else if (R >= 1 && R <= kTileMaxR &&
+    } else if (Q <= 8 && R >= 1 && R <= kTileMaxR &&
         make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, halo_x(R),
                      kTileTY + 2 * R, tile_g(R))) {
         ctx.before("k_blur_solve");
@@ -231,7 +233,9 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
         set_smem(k_blur_solve<Q, RR>, sm);                                                          \
         launch_pdl(k_blur_solve<Q, RR>, grid, block, sm, s, tm, Bx, By, models, mstride, ea, em, taps); \
         break;
-        switch (taps.R) { FLR_K2(1) FLR_K2(2) FLR_K2(3) FLR_K2(4) FLR_K2(5) FLR_K2(6) FLR_K2(7) FLR_K2(8) }
+        if constexpr (Q <= 8) {
+            switch (taps.R) { FLR_K2(1) FLR_K2(2) FLR_K2(3) FLR_K2(4) FLR_K2(5) FLR_K2(6) FLR_K2(7) FLR_K2(8) }
+        }
 #undef FLR_K2
     } else {
         ctx.before("k_hblur");

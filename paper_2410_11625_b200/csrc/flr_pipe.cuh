@@ -56,6 +56,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity)
     }
 }
 
+// Producer side of a warp-specialised ring, before a TMA write into a stage the consumers
+// have read: a generic -> async proxy fence (conservative; measured free, FLR_WS_NO_PROXY_FENCE
+// drops it for experiments).
+__device__ __forceinline__ void ws_proxy_fence()
+{
+#ifndef FLR_WS_NO_PROXY_FENCE
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ long long gtimer()
 {
     long long t;

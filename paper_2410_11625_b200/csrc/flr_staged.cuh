@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(128) k_unshift(int Bx, int Bxp, int By, const 
     const int f = blockIdx.y;
     const int nblk_frame = Bx * By;
     if (b >= nblk_frame) return;
-    const size_t cs = (size_t)nblk_frame;
+    const size_t cs = (size_t)nblk_frame;  // input component stride (the raw field is not pitched)
     const float* in = raw + (size_t)f * Dm::KRAW * cs + b;
     const size_t co = (size_t)By * Bxp;  // output component stride (pitched rows)
     double* out = mom + (size_t)f * Dm::KM * co + (size_t)(b / Bx) * Bxp + (b % Bx);
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(128) k_unshift(int Bx, int Bxp, int By, const 
     double c[Q], u[Q];
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
-        c[j] = (double)in[(size_t)(Dm::C_SH + j) * co];
-        u[j] = (double)in[(size_t)(Dm::C_U + j) * co];
+        c[j] = (double)in[(size_t)(Dm::C_SH + j) * cs];
+        u[j] = (double)in[(size_t)(Dm::C_U + j) * cs];
     }
     out[0] = n;
 #pragma unroll
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(128) k_unshift(int Bx, int Bxp, int By, const 
 #pragma unroll
         for (int j = i; j < Q; ++j) {
             const int k = Dm::s_idx(i, j);
-            double s = (double)in[(size_t)k * co];
+            double s = (double)in[(size_t)k * cs];
             s = fma(c[i], u[j], s);
             s = fma(c[j], u[i], s);
             s = fma(n * c[i], c[j], s);
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(128) k_unshift(int Bx, int Bxp, int By, const 
     double yc[3];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
-        yc[cc] = (double)in[(size_t)(Dm::C_Y + cc) * co];
+        yc[cc] = (double)in[(size_t)(Dm::C_Y + cc) * cs];
         out[(size_t)(Dm::C_Y + cc) * co] = yc[cc];
     }
 #pragma unroll
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(128) k_unshift(int Bx, int Bxp, int By, const 
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) {
             const int k = Dm::C_XY + j * 3 + cc;
-            out[(size_t)k * co] = fma(c[j], yc[cc], (double)in[(size_t)k * co]);
+            out[(size_t)k * co] = fma(c[j], yc[cc], (double)in[(size_t)k * cs]);
         }
 }
 

@@ -128,3 +128,16 @@ def test_binding_refuses_cpu_tensors():
     y = torch.zeros(1, 3, 8, 8)
     with pytest.raises(ValueError):
         flr.denoise(g, y)
+
+
+def test_solver_field_validated(L):
+    """flr_params.solver: APPENDIX (default) or TIKHONOV; anything else is rejected
+    before any launch."""
+    import paper_2410_11625_b200 as flr
+
+    p = flr.Params()
+    L.flr_default_params(ctypes.byref(p))
+    assert p.solver == flr.SOLVER_APPENDIX
+    for s, ok in ((0, True), (1, True), (2, False), (-1, False)):
+        p.solver = s
+        assert (L.flr_effective_radius(ctypes.byref(p)) >= 0) == ok

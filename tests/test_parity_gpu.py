@@ -107,6 +107,17 @@ def test_odd_sizes(flr, oracle_mod, W, H):
     assert_parity(out, ref, f"{W}x{H}")
 
 
+@pytest.mark.parametrize("block", [1, 2, 4, 16])
+@pytest.mark.parametrize("W,H", [(37, 23), (65, 9), (130, 66)])
+def test_odd_sizes_every_block(flr, oracle_mod, W, H, block):
+    """Odd block-grid widths for every block size: the D < 4 moment path stages an
+    unpitched raw field before the pitched fp64 one (a stride mix-up there once broke
+    odd Bx only)."""
+    G, Y = _inputs(W, H, 4, 3250 + W + block)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y, block=block, sigma=max(2.5, 1.25 * block))
+    assert_parity(out, ref, f"{W}x{H} block={block}")
+
+
 @pytest.mark.parametrize("radius", [1, 3, 5, 8, 10])
 def test_sweep_radius(flr, oracle_mod, radius):
     G, Y = _inputs(128, 96, 8, 3300 + radius)
