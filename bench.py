@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every step from Python")
     ap.add_argument("--check", action="store_true", help="parity-check one frame against the oracle")
+    ap.add_argument("--guides", choices=["f32", "f16"], default="f32",
+                    help="guide plane precision (f16: the fp16 guide network's output, SURVEY f2)")
     return ap.parse_args()
 
 
@@ -78,25 +80,29 @@ def out_pixels(cfg):
 
 def min_bytes_per_frame(cfg):
     """Algorithmic bytes: fp32 input planes read once + output written once."""
-    Q, W, H, U = cfg["Q"], cfg["W"], cfg["H"], cfg["upsample"]
+    Q, W, H, U, gb = cfg["Q"], cfg["W"], cfg["H"], cfg["upsample"], cfg.get("gbytes", 4)
     lo = W * H
     hi = lo * U * U
     if U == 1:
-        return (Q + 3 + 3) * 4 * lo
-    return (Q + 3) * 4 * lo + Q * 4 * hi + 3 * 4 * hi
+        return (Q * gb + (3 + 3) * 4) * lo
+    return (Q * gb + 3 * 4) * lo + Q * gb * hi + 3 * 4 * hi
+
+
+def _fit_bytes(c):  # Q guide planes + 3 radiance planes read once
+    return (c["Q"] * c.get("gbytes", 4) + 3 * 4) * c["W"] * c["H"]
+
+
+def _apply_bytes(c):  # Q guide planes read + 3 output planes written once
+    return (c["Q"] * c.get("gbytes", 4) + 3 * 4) * out_pixels(c)
 
 
 KERNEL_BYTES = {
     # algorithmic bytes per frame of each launch: the full-resolution planes it must read + write
-    "k_fit_moments": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
-    "k_fit_stream": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
-    "k_fit_ldg": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
-    "k_apply_stream": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
-    "k_apply_tile": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
-    "k_apply_px": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
+    "k_fit_moments": _fit_bytes, "k_fit_stream": _fit_bytes, "k_fit_ldg": _fit_bytes, "k_fit_ws": _fit_bytes,
+    "k_fit_ws_f16": _fit_bytes,
+    "k_apply_stream": _apply_bytes, "k_apply_tile": _apply_bytes, "k_apply_px": _apply_bytes,
+    "k_apply_ws": _apply_bytes, "k_apply_ws_f16": _apply_bytes,
     "k_flr_fused": lambda c: min_bytes_per_frame(c),
-    "k_fit_ws": lambda c: (c["Q"] + 3) * 4 * c["W"] * c["H"],
-    "k_apply_ws": lambda c: (c["Q"] + 3) * 4 * out_pixels(c),
 }
 
 
@@ -311,7 +317,9 @@ def run_flr(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     W, H, Q, D, U, sigma = cfg["W"], cfg["H"], cfg["Q"], cfg["block"], cfg["upsample"], cfg["sigma"]
     F = args.frames_per_step or (32 if args.config == "c5" else 1)
-    frame_in_bytes = (Q + 3) * 4 * W * H + (Q * 4 * W * H * U * U if U > 1 else 0)
+    half = args.guides == "f16"
+    gbytes = cfg["gbytes"]
+    frame_in_bytes = (Q * gbytes + 3 * 4) * W * H + (Q * gbytes * W * H * U * U if U > 1 else 0)
     pool = args.pool or max(2, math.ceil(2.5 * L2_BYTES / (frame_in_bytes * F)))
     R = flr.effective_radius(block=D, upsample=U, sigma=sigma)
 
@@ -330,6 +338,9 @@ def run_flr(args, cfg, rank, world, local_rank):
             gl.append(torch.stack([t[0] for t in trip]).contiguous())
             yl.append(torch.stack([t[1] for t in trip]).contiguous())
             gh.append(torch.stack([t[2] for t in trip]).contiguous())
+    if half:  # the guide network's fp16 planes: converted once, before the timed region
+        gl = [g.to(torch.float16) for g in gl]
+        gh = [g.to(torch.float16) for g in gh]
     torch.cuda.synchronize()
     den = flr.Denoiser(F, Q, W, H, device=dev, block=D, upsample=U, sigma=sigma, variant=args.variant)
     outs = [torch.empty_like(den.out) for _ in range(2)]
@@ -349,12 +360,12 @@ def run_flr(args, cfg, rank, world, local_rank):
         from tests.parity import parity_report
 
         o = call(0).cpu().numpy()
-        g0 = gl[0].cpu().numpy()
+        g0 = gl[0].float().cpu().numpy()
         y0 = yl[0].cpu().numpy()
         if U == 1:
             ref = oracle.denoise(g0, y0, D=D, sigma=sigma, R=R)
         else:
-            ref = oracle.denoise_upsample(g0, y0, gh[0].cpu().numpy(), D_fit=D, U=U, sigma=sigma, R=R)
+            ref = oracle.denoise_upsample(g0, y0, gh[0].float().cpu().numpy(), D_fit=D, U=U, sigma=sigma, R=R)
         check = parity_report(o, ref)
 
     stream = torch.cuda.current_stream(dev)
@@ -460,7 +471,7 @@ def run_flr(args, cfg, rank, world, local_rank):
         h_out = den.out.cpu().pin_memory()
         d_g, d_y = torch.empty_like(gl[0]), torch.empty_like(yl[0])
         d_gh = torch.empty_like(gh[0]) if U > 1 else None
-        h2d = sum(t.numel() * 4 for t in (d_g, d_y)) + (d_gh.numel() * 4 if U > 1 else 0)
+        h2d = sum(t.numel() * t.element_size() for t in (d_g, d_y)) + (d_gh.numel() * d_gh.element_size() if U > 1 else 0)
         d2h = h_out.numel() * 4
 
         def e2e_step(i):
@@ -542,13 +553,15 @@ def run_flr(args, cfg, rank, world, local_rank):
         "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": step_ms, "ms_per_frame": step_ms / F, "frames_per_s": frames_total / (ms_max * 1e-3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (seeded procedural Lambertian scenes, rasterised guides, 1spp noise)",
+        "dtype": "f32" if not half else "f32 (fp16 guide planes)", "data": "synthetic (seeded procedural Lambertian scenes, rasterised guides, 1spp noise)",
         "config": {"workload": cfg["workload"], "W": W, "H": H, "Q": Q, "block": D, "upsample": U, "sigma": sigma,
                    "radius": R, "eps_add": 1e-5, "eps_mul": 1e-4, "frames_per_step": F, "global_batch": world * F,
                    "pool_frames": pool, "l2": f"rotating pool of {pool} distinct steps "
                    f"({pool * F * frame_in_bytes / 1e6:.0f} MB > 126 MB L2)", "graphs": use_graph,
                    "parallelism": f"frame-sharded dp{world}", "variant": args.variant,
-                   "numerics": "fp32 streams, fp64 block blur+solve"},
+                   "guides": args.guides,
+                   "numerics": "fp32 streams, fp64 block blur+solve"
+                               + ("; fp16 guide planes widened exactly to fp32 on load" if half else "")},
         "roofline": roof, "step_roofline": step_roof,
         "kernel_us": {n: (t * 1e3 if t else None) for n, t in avg_ms.items()},
         "kernel_roofline": kroof,
@@ -565,6 +578,7 @@ def run_flr(args, cfg, rank, world, local_rank):
 def main():
     args = parse()
     cfg = dict(CONFIGS[args.config])
+    cfg["gbytes"] = 2 if args.guides == "f16" else 4
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -140,6 +140,29 @@ flr_status flr_denoise_upsample(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo
                                 const flr_params* p, float* out, void* workspace,
                                 size_t workspace_bytes, flr_stream_t stream);
 
+/* Half-precision guide planes: the paper's guide network runs in fp16
+ * (P:414), so its enhanced guides X' arrive as IEEE binary16.  These entry
+ * points take guides as binary16 bit patterns (uint16_t) and otherwise behave exactly as
+ * their fp32 counterparts; every fp16 value is converted exactly to fp32 on load, so the
+ * result equals the fp32 path run on the same values widened to fp32.  Radiance, models
+ * and output stay fp32.  Only the TMA streaming kernels read fp16 planes, so they need
+ * W % 8 == 0 (fit and output widths), 16-byte aligned planes, block in {4, 8, 16} and an
+ * output block size (block * upsample) that is a multiple of 8; any other shape returns
+ * FLR_ERR_UNSUPPORTED (nothing launched).  FLR_VARIANT_FUSED is not available here.
+ * FLNR's split guides (fit on X'_model, apply X'_map) are the
+ * denoise_upsample call with p->upsample == 1 and guides_lo = X'_model,
+ * guides_hi = X'_map. */
+flr_status flr_fit_f16(int32_t n, int32_t Q, int32_t W_fit, int32_t H_fit, const uint16_t* guides_fit,
+                       const float* radiance_fit, const flr_params* p, float* models, void* workspace,
+                       size_t workspace_bytes, flr_stream_t stream);
+flr_status flr_denoise_f16(int32_t n, int32_t Q, int32_t W, int32_t H, const uint16_t* guides,
+                           const float* radiance, const flr_params* p, float* out, void* workspace,
+                           size_t workspace_bytes, flr_stream_t stream);
+flr_status flr_denoise_upsample_f16(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo, const uint16_t* guides_lo,
+                                    const float* radiance_lo, int32_t W_hi, int32_t H_hi,
+                                    const uint16_t* guides_hi, const flr_params* p, float* out, void* workspace,
+                                    size_t workspace_bytes, flr_stream_t stream);
+
 /* The paper's protocol around FLR: the renderer's indirect
  * radiance is albedo-modulated, FLR denoises the DEMODULATED signal, and the result is
  * remodulated and the noise-free direct light added:
@@ -183,6 +206,14 @@ flr_status flr_denoise_upsample_traced(int32_t n, int32_t Q, int32_t W_lo, int32
                                        const flr_params* p, float* out, void* workspace,
                                        size_t workspace_bytes, flr_stream_t stream,
                                        flr_event_trace* trace);
+flr_status flr_denoise_upsample_f16_traced(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo,
+                                           const uint16_t* guides_lo, const float* radiance_lo, int32_t W_hi,
+                                           int32_t H_hi, const uint16_t* guides_hi, const flr_params* p, float* out,
+                                           void* workspace, size_t workspace_bytes, flr_stream_t stream,
+                                           flr_event_trace* trace);
+flr_status flr_denoise_f16_traced(int32_t n, int32_t Q, int32_t W, int32_t H, const uint16_t* guides,
+                                  const float* radiance, const flr_params* p, float* out, void* workspace,
+                                  size_t workspace_bytes, flr_stream_t stream, flr_event_trace* trace);
 flr_status flr_denoise_modulated_traced(int32_t n, int32_t Q, int32_t W, int32_t H, const float* guides,
                                         const float* radiance_mod, const float* albedo, const float* direct,
                                         float albedo_floor, const flr_params* p, float* out, void* workspace,

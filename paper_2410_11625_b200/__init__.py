@@ -101,13 +101,20 @@ def lib():
                                             vp]
         L.flr_denoise_modulated_traced.argtypes = [i32, i32, i32, i32, dp, dp, dp, dp, ctypes.c_float, pp, dp,
                                                    vp, sz, vp, tp]
+        L.flr_fit_f16.argtypes = [i32, i32, i32, i32, dp, dp, pp, dp, vp, sz, vp]
+        L.flr_denoise_f16.argtypes = [i32, i32, i32, i32, dp, dp, pp, dp, vp, sz, vp]
+        L.flr_denoise_f16_traced.argtypes = [i32, i32, i32, i32, dp, dp, pp, dp, vp, sz, vp, tp]
+        L.flr_denoise_upsample_f16.argtypes = [i32, i32, i32, i32, dp, dp, i32, i32, dp, pp, dp, vp, sz, vp]
+        L.flr_denoise_upsample_f16_traced.argtypes = [i32, i32, i32, i32, dp, dp, i32, i32, dp, pp, dp, vp, sz,
+                                                      vp, tp]
         L.flr_last_launch_count.argtypes = []
         L.flr_last_launch_count.restype = i32
         L.flr_last_launch_name.argtypes = [i32]
         L.flr_last_launch_name.restype = ctypes.c_char_p
         for f in ("flr_workspace_size", "flr_fit", "flr_apply", "flr_denoise", "flr_denoise_upsample",
                   "flr_denoise_traced", "flr_denoise_upsample_traced", "flr_denoise_modulated",
-                  "flr_denoise_modulated_traced"):
+                  "flr_denoise_modulated_traced", "flr_fit_f16", "flr_denoise_f16", "flr_denoise_f16_traced",
+                  "flr_denoise_upsample_f16", "flr_denoise_upsample_f16_traced"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -151,14 +158,14 @@ def _torch():
     return torch
 
 
-def _frames(t, name, C=None):
+def _frames(t, name, C=None, half_ok=False):
     torch = _torch()
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
-    if t.dtype != torch.float32:
-        raise TypeError(f"{name} must be float32")
+    if t.dtype != torch.float32 and not (half_ok and t.dtype == torch.float16):
+        raise TypeError(f"{name} must be float32" + (" or float16" if half_ok else ""))
     if t.dim() == 3:
         t = t.unsqueeze(0)
     if t.dim() != 4:
@@ -191,9 +198,10 @@ def _ptr(t):
 
 def fit(guides, radiance, *, block=8, upsample=1, sigma=10.0, radius=0, eps_add=1e-5,
         eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None, workspace=None):
-    """Per-block raw-basis models [n, By, Bx, Q+1, 3]."""
+    """Per-block raw-basis models [n, By, Bx, Q+1, 3].
+    float16 guides (the fp16 guide network's output) take the fp16 streaming path."""
     torch = _torch()
-    g = _frames(guides, "guides")
+    g = _frames(guides, "guides", half_ok=True)
     y = _frames(radiance, "radiance", 3)
     n, Q, H, W = g.shape
     if tuple(y.shape) != (n, 3, H, W):
@@ -205,8 +213,9 @@ def fit(guides, radiance, *, block=8, upsample=1, sigma=10.0, radius=0, eps_add=
     ws_bytes = workspace_size(n, Q, W, H, block=block, upsample=upsample, sigma=sigma, radius=radius,
                               eps_add=eps_add, eps_mul=eps_mul, variant=variant)
     ws = _workspace(ws_bytes, g.device, workspace)
-    _check(lib().flr_fit(n, Q, W, H, _ptr(g), _ptr(y), ctypes.byref(p), _ptr(out), _ptr(ws),
-                         ws.numel() * ws.element_size(), _stream_ptr(g.device)), "flr_fit")
+    fn = lib().flr_fit_f16 if g.dtype == torch.float16 else lib().flr_fit
+    _check(fn(n, Q, W, H, _ptr(g), _ptr(y), ctypes.byref(p), _ptr(out), _ptr(ws),
+              ws.numel() * ws.element_size(), _stream_ptr(g.device)), "flr_fit")
     return out
 
 
@@ -232,9 +241,10 @@ def apply(models, guides, block_out, *, out=None):
 
 def denoise(guides, radiance, *, block=8, sigma=10.0, radius=0, eps_add=1e-5, eps_mul=1e-4,
             variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None, workspace=None):
-    """FLR denoise: fit + apply with the same guides.  [n,Q,H,W], [n,3,H,W] -> [n,3,H,W]."""
+    """FLR denoise: fit + apply with the same guides.  [n,Q,H,W], [n,3,H,W] -> [n,3,H,W].
+    Guides may be float16 (fp16 streaming path)."""
     torch = _torch()
-    g = _frames(guides, "guides")
+    g = _frames(guides, "guides", half_ok=True)
     y = _frames(radiance, "radiance", 3)
     n, Q, H, W = g.shape
     if tuple(y.shape) != (n, 3, H, W):
@@ -245,19 +255,24 @@ def denoise(guides, radiance, *, block=8, sigma=10.0, radius=0, eps_add=1e-5, ep
     ws_bytes = workspace_size(n, Q, W, H, block=block, sigma=sigma, radius=radius, eps_add=eps_add,
                               eps_mul=eps_mul, variant=variant)
     ws = _workspace(ws_bytes, g.device, workspace)
-    _check(lib().flr_denoise(n, Q, W, H, _ptr(g), _ptr(y), ctypes.byref(p), _ptr(out), _ptr(ws),
-                             ws.numel() * ws.element_size(), _stream_ptr(g.device)), "flr_denoise")
+    fn = lib().flr_denoise_f16 if g.dtype == torch.float16 else lib().flr_denoise
+    _check(fn(n, Q, W, H, _ptr(g), _ptr(y), ctypes.byref(p), _ptr(out), _ptr(ws),
+              ws.numel() * ws.element_size(), _stream_ptr(g.device)), "flr_denoise")
     return out
 
 
 def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, sigma=10.0, radius=0,
                      eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None,
                      workspace=None):
-    """Joint denoise + upsample: fit on low-res radiance/guides, apply with hi-res guides."""
+    """Joint denoise + upsample: fit on low-res radiance/guides, apply with hi-res guides.
+    With upsample=1 this is FLNR's split-guide call (fit on X'_model, apply X'_map).
+    Both guide sets float32, or both float16 (fp16 streaming path)."""
     torch = _torch()
-    g = _frames(guides_lo, "guides_lo")
+    g = _frames(guides_lo, "guides_lo", half_ok=True)
     y = _frames(radiance_lo, "radiance_lo", 3)
-    gh = _frames(guides_hi, "guides_hi")
+    gh = _frames(guides_hi, "guides_hi", half_ok=True)
+    if g.dtype != gh.dtype:
+        raise TypeError("guides_lo and guides_hi must have the same dtype")
     n, Q, H, W = g.shape
     Hh, Wh = int(gh.shape[2]), int(gh.shape[3])
     if tuple(y.shape) != (n, 3, H, W) or gh.shape[0] != n or gh.shape[1] != Q:
@@ -268,9 +283,9 @@ def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, 
     ws_bytes = workspace_size(n, Q, W, H, block=block, upsample=upsample, sigma=sigma, radius=radius,
                               eps_add=eps_add, eps_mul=eps_mul, variant=variant)
     ws = _workspace(ws_bytes, g.device, workspace)
-    _check(lib().flr_denoise_upsample(n, Q, W, H, _ptr(g), _ptr(y), Wh, Hh, _ptr(gh), ctypes.byref(p),
-                                      _ptr(out), _ptr(ws), ws.numel() * ws.element_size(),
-                                      _stream_ptr(g.device)), "flr_denoise_upsample")
+    fn = lib().flr_denoise_upsample_f16 if g.dtype == torch.float16 else lib().flr_denoise_upsample
+    _check(fn(n, Q, W, H, _ptr(g), _ptr(y), Wh, Hh, _ptr(gh), ctypes.byref(p), _ptr(out), _ptr(ws),
+              ws.numel() * ws.element_size(), _stream_ptr(g.device)), "flr_denoise_upsample")
     return out
 
 
@@ -325,6 +340,18 @@ class Denoiser:
         ws = self.workspace
         tr = ctypes.byref(trace) if trace is not None else None
         gh = guides if guides_hi is None else guides_hi
+        if guides.dtype == torch.float16:  # fp16 guide planes (flr_*_f16)
+            if guides_hi is None:
+                st = self._L.flr_denoise_f16_traced(self.n, self.Q, self.W, self.H, guides.data_ptr(),
+                                                    radiance.data_ptr(), ctypes.byref(self.params), out.data_ptr(),
+                                                    ws.data_ptr(), ws.numel(), s, tr)
+            else:
+                st = self._L.flr_denoise_upsample_f16_traced(self.n, self.Q, self.W, self.H, guides.data_ptr(),
+                                                             radiance.data_ptr(), self.W * self.U, self.H * self.U,
+                                                             gh.data_ptr(), ctypes.byref(self.params),
+                                                             out.data_ptr(), ws.data_ptr(), ws.numel(), s, tr)
+            _check(st, "flr_denoise_f16")
+            return out
         st = self._L.flr_denoise_upsample_traced(self.n, self.Q, self.W, self.H, guides.data_ptr(),
                                                  radiance.data_ptr(), self.W * self.U, self.H * self.U,
                                                  gh.data_ptr(), ctypes.byref(self.params), out.data_ptr(),

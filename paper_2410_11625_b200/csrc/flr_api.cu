@@ -146,7 +146,7 @@ flr_status check_ws(int n, int Q, int W, int H, const flr_params* p, void* ws, s
 
 // fit into `models` with `mstride` floats per block; arguments already validated
 flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, const flr_params* p,
-                  float* models, int mstride, void* ws, LaunchCtx& ctx)
+                  float* models, int mstride, void* ws, LaunchCtx& ctx, bool hg = false)
 {
     const int D = p->block;
     const int Bx = cdiv(W, D), By = cdiv(H, D);
@@ -160,7 +160,7 @@ flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, co
     ctx.wave_flags = wave ? (int*)(base + L.flags) : nullptr;
     FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, G, Y, (float*)(base + L.raw),
                                       (double*)(base + L.mom), (double*)(base + L.hb), models,
-                                      mstride, p->eps_add, solver_eps_mul(p), taps, ctx)));
+                                      mstride, p->eps_add, solver_eps_mul(p), taps, ctx, nullptr, 0.f, hg)));
     return FLR_OK;
 }
 
@@ -283,12 +283,17 @@ flr_status flr_apply(int32_t n, int32_t Q, int32_t W_out, int32_t H_out, int32_t
     return finish(ctx, nullptr);
 }
 
-flr_status flr_denoise_upsample_traced(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo,
-                                       const float* guides_lo, const float* radiance_lo, int32_t W_hi,
-                                       int32_t H_hi, const float* guides_hi, const flr_params* p,
-                                       float* out, void* workspace, size_t workspace_bytes,
-                                       flr_stream_t stream, flr_event_trace* trace)
+}  // extern "C"
+
+namespace {
+// fit on (guides_lo, radiance_lo) + apply with guides_hi; hg: both guide sets are fp16
+flr_status denoise_upsample_impl(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo, const void* guides_lo_,
+                                 const float* radiance_lo, int32_t W_hi, int32_t H_hi, const void* guides_hi_,
+                                 const flr_params* p, float* out, void* workspace, size_t workspace_bytes,
+                                 flr_stream_t stream, flr_event_trace* trace, bool hg)
 {
+    const float* guides_lo = (const float*)guides_lo_;
+    const float* guides_hi = (const float*)guides_hi_;
     flr_status st = check_fit_args(n, Q, W_lo, H_lo, guides_lo, radiance_lo, p);
     if (st) return st;
     if (!guides_hi || !out) return FLR_ERR_INVALID_VALUE;
@@ -318,12 +323,85 @@ flr_status flr_denoise_upsample_traced(int32_t n, int32_t Q, int32_t W_lo, int32
         if (done) return finish(ctx, trace);
         if (p->variant == FLR_VARIANT_FUSED) return FLR_ERR_UNSUPPORTED;
     }
-    if ((st = do_fit(n, Q, W_lo, H_lo, guides_lo, radiance_lo, p, models, ms, workspace, ctx)))
-        return st;
     const int Dout = D * p->upsample;
-    FLR_DISPATCH_Q(Q, (launch_apply<QQ>(n, W_hi, H_hi, Dout, Bx, By, models, ms, guides_hi, out, ctx)));
+    if (hg && (!half_guides_fit_ok(D, W_lo, guides_lo, radiance_lo) ||
+               !half_guides_apply_ok(Dout, W_hi, models, guides_hi, out)))
+        return FLR_ERR_UNSUPPORTED;
+    if ((st = do_fit(n, Q, W_lo, H_lo, guides_lo, radiance_lo, p, models, ms, workspace, ctx, hg)))
+        return st;
+    FLR_DISPATCH_Q(Q, (launch_apply<QQ>(n, W_hi, H_hi, Dout, Bx, By, models, ms, guides_hi, out, ctx, nullptr,
+                                        nullptr, hg)));
     return finish(ctx, trace);
 }
+}  // namespace
+
+extern "C" {
+
+flr_status flr_denoise_upsample_traced(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo,
+                                       const float* guides_lo, const float* radiance_lo, int32_t W_hi,
+                                       int32_t H_hi, const float* guides_hi, const flr_params* p,
+                                       float* out, void* workspace, size_t workspace_bytes,
+                                       flr_stream_t stream, flr_event_trace* trace)
+{
+    return denoise_upsample_impl(n, Q, W_lo, H_lo, guides_lo, radiance_lo, W_hi, H_hi, guides_hi, p, out,
+                                 workspace, workspace_bytes, stream, trace, false);
+}
+
+flr_status flr_denoise_upsample_f16_traced(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo,
+                                           const uint16_t* guides_lo, const float* radiance_lo, int32_t W_hi,
+                                           int32_t H_hi, const uint16_t* guides_hi, const flr_params* p, float* out,
+                                           void* workspace, size_t workspace_bytes, flr_stream_t stream,
+                                           flr_event_trace* trace)
+{
+    if (p && p->variant == FLR_VARIANT_FUSED) return FLR_ERR_UNSUPPORTED;
+    return denoise_upsample_impl(n, Q, W_lo, H_lo, guides_lo, radiance_lo, W_hi, H_hi, guides_hi, p, out,
+                                 workspace, workspace_bytes, stream, trace, true);
+}
+
+flr_status flr_denoise_upsample_f16(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo, const uint16_t* guides_lo,
+                                    const float* radiance_lo, int32_t W_hi, int32_t H_hi,
+                                    const uint16_t* guides_hi, const flr_params* p, float* out, void* workspace,
+                                    size_t workspace_bytes, flr_stream_t stream)
+{
+    return flr_denoise_upsample_f16_traced(n, Q, W_lo, H_lo, guides_lo, radiance_lo, W_hi, H_hi, guides_hi, p, out,
+                                           workspace, workspace_bytes, stream, nullptr);
+}
+
+flr_status flr_denoise_f16_traced(int32_t n, int32_t Q, int32_t W, int32_t H, const uint16_t* guides,
+                                  const float* radiance, const flr_params* p, float* out, void* workspace,
+                                  size_t workspace_bytes, flr_stream_t stream, flr_event_trace* trace)
+{
+    if (p && (p->upsample != 1 || p->variant == FLR_VARIANT_FUSED))
+        return p->upsample != 1 ? FLR_ERR_INVALID_VALUE : FLR_ERR_UNSUPPORTED;
+    return denoise_upsample_impl(n, Q, W, H, guides, radiance, W, H, guides, p, out, workspace, workspace_bytes,
+                                 stream, trace, true);
+}
+
+flr_status flr_denoise_f16(int32_t n, int32_t Q, int32_t W, int32_t H, const uint16_t* guides,
+                           const float* radiance, const flr_params* p, float* out, void* workspace,
+                           size_t workspace_bytes, flr_stream_t stream)
+{
+    return flr_denoise_f16_traced(n, Q, W, H, guides, radiance, p, out, workspace, workspace_bytes, stream,
+                                  nullptr);
+}
+
+flr_status flr_fit_f16(int32_t n, int32_t Q, int32_t W_fit, int32_t H_fit, const uint16_t* guides_fit,
+                       const float* radiance_fit, const flr_params* p, float* models, void* workspace,
+                       size_t workspace_bytes, flr_stream_t stream)
+{
+    flr_status st = check_fit_args(n, Q, W_fit, H_fit, guides_fit, radiance_fit, p);
+    if (st) return st;
+    if (!models) return FLR_ERR_INVALID_VALUE;
+    if (!aligned(models, 4)) return FLR_ERR_ALIGNMENT;
+    if ((st = check_ws(n, Q, W_fit, H_fit, p, workspace, workspace_bytes))) return st;
+    if (!half_guides_fit_ok(p->block, W_fit, guides_fit, radiance_fit)) return FLR_ERR_UNSUPPORTED;
+    LaunchCtx ctx = make_ctx(stream, nullptr);
+    if ((st = do_fit(n, Q, W_fit, H_fit, (const float*)guides_fit, radiance_fit, p, models, 3 * (Q + 1), workspace,
+                     ctx, true)))
+        return st;
+    return finish(ctx, nullptr);
+}
+
 
 flr_status flr_denoise_upsample(int32_t n, int32_t Q, int32_t W_lo, int32_t H_lo,
                                 const float* guides_lo, const float* radiance_lo, int32_t W_hi,

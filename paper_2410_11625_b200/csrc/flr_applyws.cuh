@@ -10,6 +10,8 @@
 // pixel quad of the Q guide planes, and applies I = (1 - t_x) x~.A_y(i0) + t_x x~.A_y(i1)
 // with packed fp32x2 FMAs, streaming the 3 output planes out (st.global.cs).
 #pragma once
+#include <cuda_fp16.h>
+
 #include "flr_stream.cuh"
 
 namespace flr {
@@ -18,11 +20,13 @@ constexpr int kApplyWsNC = 7;  // consumer warps (+1 producer = 8 warps, 255-reg
 constexpr int kApplyWsS = 4;   // guide-row stages per consumer
 constexpr int kApplyWsM = 2;   // model stages per consumer
 
-template <int Q, bool MOD = false>
+template <int Q, bool MOD = false, bool HG = false>
 struct ApplyWsCfg {
     using SD = StreamDims<Q>;
-    // floats per row stage: Q guide planes (+ 3 albedo and 3 direct-light planes)
-    static constexpr int ROWF = (Q + (MOD ? 6 : 0)) * kSeg;
+    // floats per row stage: Q guide planes (fp32, or fp16 when HG) (+ 3 albedo and 3
+    // direct-light planes)
+    static constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats per guide plane
+    static constexpr int ROWF = Q * GF + (MOD ? 6 : 0) * kSeg;
     static constexpr int MODF = 2 * kApplyNCol * SD::MS;  // floats per model stage
     // as many guide-row stages (<= kApplyWsS) as fit in 227 KB with 7 consumers
     static constexpr int fit_stages(int s)
@@ -42,10 +46,11 @@ struct ApplyWsCfg {
     static_assert(FITS || MOD, "apply pipeline exceeds 227 KB of shared memory");
 };
 
-template <int Q, bool MOD = false>
-__global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(const __grid_constant__ ApplyArgs a, int n)
+template <int Q, bool MOD = false, bool HG = false>
+__global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws(const __grid_constant__ ApplyArgs a, int n)
 {
-    using C = ApplyWsCfg<Q, MOD>;
+    using C = ApplyWsCfg<Q, MOD, HG>;
+    constexpr int GF = C::GF, RO = Q * GF;  // RO: first remodulation plane (floats)
     using SD = StreamDims<Q>;
     constexpr int NC = C::NC, S = C::S, SM = C::SM, MS = SD::MS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(con
             int pit = it, py0 = y;
             for (; kr < S && pit < nitems && py0 < g.y1; ++kr, ++py0) {
                 ws_proxy_fence();
-                apply_issue_row<Q, MOD>(a, g, f, py0, rows_st + kr * C::ROWF, &rfull[kr], pg);
+                apply_issue_row<Q, MOD, HG>(a, g, f, py0, rows_st + kr * C::ROWF, &rfull[kr], pg);
             }
             pre = kr;
         }
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(con
                 const int s = kr % S;
                 if (kr < S || mbar_test_wait(&rempty[s], ((kr / S) - 1) & 1)) {
                     ws_proxy_fence();
-                    apply_issue_row<Q, MOD>(a, g, f, y, rows_st + s * C::ROWF, &rfull[s], pg);
+                    apply_issue_row<Q, MOD, HG>(a, g, f, y, rows_st + s * C::ROWF, &rfull[s], pg);
                     ++kr;
                     if (++y == g.y1) {
                         it += GW;
@@ -198,7 +203,15 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(con
             float gq[Q][4];
 #pragma unroll
             for (int j = 0; j < Q; ++j) {
-                const float4 v = reinterpret_cast<const float4*>(st + j * kSeg)[lane];
+                float4 v;
+                if (HG) {  // 4 fp16 guides -> fp32 (exact)
+                    const uint2 hv = reinterpret_cast<const uint2*>(st + j * GF)[lane];
+                    const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&hv.x));
+                    const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&hv.y));
+                    v = make_float4(lo.x, lo.y, hi.x, hi.y);
+                } else {
+                    v = reinterpret_cast<const float4*>(st + j * kSeg)[lane];
+                }
                 gq[j][0] = v.x; gq[j][1] = v.y; gq[j][2] = v.z; gq[j][3] = v.w;
             }
             float m0[MS], m1[MS];
@@ -227,9 +240,9 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD>::THREADS, 1) k_apply_ws(con
             if (MOD) {  // remodulation and direct light: out = albedo * I + direct (R21)
 #pragma unroll
                 for (int cc = 0; cc < 3; ++cc) {
-                    const float4 al = reinterpret_cast<const float4*>(st + (Q + cc) * kSeg)[lane];
+                    const float4 al = reinterpret_cast<const float4*>(st + RO + cc * kSeg)[lane];
                     float4 dl = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (a.has_direct) dl = reinterpret_cast<const float4*>(st + (Q + 3 + cc) * kSeg)[lane];
+                    if (a.has_direct) dl = reinterpret_cast<const float4*>(st + RO + (3 + cc) * kSeg)[lane];
                     o[cc][0] = fmaf(al.x, o[cc][0], dl.x);
                     o[cc][1] = fmaf(al.y, o[cc][1], dl.y);
                     o[cc][2] = fmaf(al.z, o[cc][2], dl.z);

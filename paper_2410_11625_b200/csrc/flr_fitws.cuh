@@ -13,6 +13,8 @@
 // added once per item.  Sums are taken about the block's top-left pixel c (design rule
 // H1) and un-shifted to fp64 in the epilogue (FitAcc::store's algebra).
 #pragma once
+#include <cuda_fp16.h>
+
 #include "flr_persist.cuh"
 
 namespace flr {
@@ -23,10 +25,12 @@ constexpr int kFitWsNC = 7;  // consumer warps (+1 producer = 8 warps: 2 per SMS
 #endif
 constexpr int kFitWsS = FLR_FITWS_S;  // ring stages per consumer
 
-template <int Q, bool MOD = false>
+template <int Q, bool MOD = false, bool HG = false>
 struct FitWsCfg {
-    // floats per stage (one pixel row): Q guide planes, 3 radiance planes (+ 3 albedo planes)
-    static constexpr int STG = StreamDims<Q>::STG_FIT + (MOD ? 3 * kSeg : 0);
+    // floats per stage (one pixel row): Q guide planes (fp32, or fp16 when HG), 3 radiance
+    // planes (+ 3 albedo planes)
+    static constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats per guide plane
+    static constexpr int STG = Q * GF + (3 + (MOD ? 3 : 0)) * kSeg;
     // as many stages (<= kFitWsS) as fit in 227 KB with 7 consumers
     static constexpr int fit_stages(int s)
     {
@@ -84,17 +88,19 @@ __device__ __forceinline__ void fold_pairs(const f2 (&in)[N], float (&out)[N], i
 }
 
 // the rows of one item for one consumer warp (k: rows consumed so far by this warp)
-template <int Q, int D, bool EDGE, bool MOD>
+template <int Q, int D, bool EDGE, bool MOD, bool HG>
 __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], const float* ring, uint64_t* full,
                                             uint64_t* empty, int& k, int rows, int lane, int lb0, int x0, int W,
                                             float afloor)
 {
-    constexpr int S = FitWsCfg<Q, MOD>::S, STG = FitWsCfg<Q, MOD>::STG;
+    using C = FitWsCfg<Q, MOD, HG>;
+    constexpr int S = C::S, STG = C::STG, GF = C::GF, RO = Q * GF;  // RO: radiance offset (floats)
     {  // the block shift c = its top-left pixel (first row of the item)
         mbar_wait(&full[k % S], (k / S) & 1);
         const float* st = ring + (k % S) * STG;
 #pragma unroll
-        for (int j = 0; j < Q; ++j) cs[j] = st[j * kSeg + lb0];
+        for (int j = 0; j < Q; ++j)
+            cs[j] = HG ? __half2float(reinterpret_cast<const __half*>(st + j * GF)[lb0]) : st[j * kSeg + lb0];
     }
 #pragma unroll 1  // keep the row body resident in the instruction cache
     for (int rr = 0; rr < rows; ++rr, ++k) {
@@ -105,13 +111,20 @@ __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], c
         for (int h = 0; h < 2; ++h) {
             f2 d[Q], y[3];
 #pragma unroll
-            for (int j = 0; j < Q; ++j) d[j] = reinterpret_cast<const f2*>(st + j * kSeg)[2 * lane + h];
+            for (int j = 0; j < Q; ++j) {
+                if (HG) {  // fp16 guide pair -> fp32 (exact)
+                    const float2 v = __half22float2(reinterpret_cast<const __half2*>(st + j * GF)[2 * lane + h]);
+                    d[j] = pk2(v.x, v.y);
+                } else {
+                    d[j] = reinterpret_cast<const f2*>(st + j * kSeg)[2 * lane + h];
+                }
+            }
 #pragma unroll
-            for (int c = 0; c < 3; ++c) y[c] = reinterpret_cast<const f2*>(st + (Q + c) * kSeg)[2 * lane + h];
+            for (int c = 0; c < 3; ++c) y[c] = reinterpret_cast<const f2*>(st + RO + c * kSeg)[2 * lane + h];
             if (MOD) {  // demodulation y = radiance / max(albedo, floor) (R20)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const f2 al = reinterpret_cast<const f2*>(st + (Q + 3 + c) * kSeg)[2 * lane + h];
+                    const f2 al = reinterpret_cast<const f2*>(st + RO + (3 + c) * kSeg)[2 * lane + h];
                     y[c] = pk2(lo2(y[c]) * __frcp_rn(fmaxf(lo2(al), afloor)),
                                hi2(y[c]) * __frcp_rn(fmaxf(hi2(al), afloor)));
                 }
@@ -134,10 +147,10 @@ __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], c
     }
 }
 
-template <int Q, int D, bool MOD = false>
-__global__ void __launch_bounds__(FitWsCfg<Q, MOD>::THREADS, 1) k_fit_ws(const __grid_constant__ FitArgs a, int n)
+template <int Q, int D, bool MOD = false, bool HG = false>
+__global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(const __grid_constant__ FitArgs a, int n)
 {
-    using C = FitWsCfg<Q, MOD>;
+    using C = FitWsCfg<Q, MOD, HG>;
     using Dm = Dims<Q>;
     constexpr int NC = C::NC, S = C::S, STG = C::STG, DQ = D / 4;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -180,7 +193,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD>::THREADS, 1) k_fit_ws(const _
             const int slot = k % S;
             if (it < nitems && (k < S || mbar_test_wait(&empty[c * S + slot], ((k / S) - 1) & 1))) {
                 ws_proxy_fence();
-                fit_issue_row<Q, D, MOD>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
+                fit_issue_row<Q, D, MOD, HG>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
                                     pg, py);
                 ++k;
                 if (++row == rows) {
@@ -205,10 +218,10 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD>::THREADS, 1) k_fit_ws(const _
         FitAccPix<Q> acc;
         acc.zero();
         if (sg * kSeg + kSeg > a.W)  // segment reaches past the image
-            fit_ws_rows<Q, D, true, MOD>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
+            fit_ws_rows<Q, D, true, MOD, HG>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
                                          a.afloor);
         else
-            fit_ws_rows<Q, D, false, MOD>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
+            fit_ws_rows<Q, D, false, MOD, HG>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
                                           a.afloor);
         // epilogue: fold, then un-shift to fp64 and store (lanes of a block split the components)
         float u[Q], sv[Dm::NS], yc[3], xy[3 * Q];

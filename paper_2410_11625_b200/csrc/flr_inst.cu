@@ -22,13 +22,13 @@ namespace flr {
 // dev build: this Q is compiled out (see build.py FLR_QS); calls report FLR_ERR_UNSUPPORTED
 template <int Q>
 void launch_fit(int, int, int, int, int, int, const float*, const float*, float*, double*, double*, float*,
-                int, double, double, const Taps&, LaunchCtx& ctx, const float*, float)
+                int, double, double, const Taps&, LaunchCtx& ctx, const float*, float, bool)
 {
     ctx.unsupported = true;
 }
 template <int Q>
 void launch_apply(int, int, int, int, int, int, const float*, int, const float*, float*, LaunchCtx& ctx,
-                  const float*, const float*)
+                  const float*, const float*, bool)
 {
     ctx.unsupported = true;
 }
@@ -74,8 +74,21 @@ static int num_sms()
 // returns true when the TMA-ring kernel ran with `done` row counters (K2 may then wait per row)
 template <int Q, int D>
 static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
-                      int* done, cudaStream_t s, const float* A, float afloor)
+                      int* done, cudaStream_t s, const float* A, float afloor, bool hg)
 {
+    if (hg) {  // fp16 guide planes: the warp-specialised kernel with a half-width guide stage
+        FitArgs a;
+        std::memset(&a, 0, sizeof(a));
+        if (!make_tmap_planes_f16(&a.tg, G, W, H, n * Q, kSeg, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kSeg, 3))
+            return false;
+        a.mom = mom;
+        a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
+        using C = FitWsCfg<Q, false, true>;
+        const int grid = min(num_sms(), cdiv(n * By * a.nseg, C::NC));
+        set_smem(k_fit_ws<Q, D, false, true>, C::SMEM);
+        launch_pdl(k_fit_ws<Q, D, false, true>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+        return false;
+    }
     if (A) {  // modulated fit: the warp-specialised kernel with the albedo planes in its ring
         FitArgs a;
         if (!make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kSeg, 3) ||
@@ -140,7 +153,7 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
 template <int Q>
 void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, const float* Y,
                 float* raw, double* mom, double* hb, float* models, int mstride, double ea,
-                double em, const Taps& taps, LaunchCtx& ctx, const float* A, float afloor)
+                double em, const Taps& taps, LaunchCtx& ctx, const float* A, float afloor, bool hg)
 {
     const cudaStream_t s = ctx.s;
     // wavefront flags: fit_done [n][By] | k2_done [n][ceil(By / kK2TY)]
@@ -151,10 +164,10 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     bool fit_signals = false;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
-        ctx.before(A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : std::getenv("FLR_FIT_RING") ? "k_fit_stream" : "k_fit_ws");
-        if (D == 4) fit_signals = launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor);
-        else if (D == 8) fit_signals = launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor);
-        else fit_signals = launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor);
+        ctx.before(hg ? "k_fit_ws_f16" : A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : std::getenv("FLR_FIT_RING") ? "k_fit_stream" : "k_fit_ws");
+        if (D == 4) fit_signals = launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg);
+        else if (D == 8) fit_signals = launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg);
+        else fit_signals = launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg);
     } else {
         ctx.before("k_moments_small");
         k_moments_small<Q><<<dim3(cdiv(Bx, 128), By, n), 128, 0, s>>>(W, H, Bx, By, D, G, Y, raw);
@@ -251,9 +264,30 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
 
 template <int Q>
 void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* models, int mstride,
-                  const float* G, float* out, LaunchCtx& ctx, const float* A, const float* Dl)
+                  const float* G, float* out, LaunchCtx& ctx, const float* A, const float* Dl, bool hg)
 {
     const cudaStream_t s = ctx.s;
+    if (hg) {  // fp16 guide planes (caller checked half_guides_apply_ok)
+        ApplyArgs a;
+        std::memset(&a, 0, sizeof(a));
+        if (mstride != Dims<Q>::MSTRIDE || !make_tmap_planes_f16(&a.tg, G, W, H, n * Q, kSeg, Q)) {
+            ctx.unsupported = true;
+            return;
+        }
+        a.models = models, a.out = out;
+        a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W, kSeg), a.nband = apply_nband(H, D, By);
+        a.nsub = 1;
+        while (D % (2 * a.nsub) == 0 && D / (2 * a.nsub) >= 4)
+            a.nsub *= 2;
+        a.reverse = 1;
+        using C = ApplyWsCfg<Q, false, true>;
+        const int items = n * a.nseg * a.nband * a.nsub;
+        const int grid = min(num_sms(), cdiv(items, C::NC));
+        ctx.before("k_apply_ws_f16");
+        set_smem(k_apply_ws<Q, false, true>, C::SMEM);
+        launch_pdl(k_apply_ws<Q, false, true>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+        return;
+    }
     if constexpr (!ApplyWsCfg<Q, true>::FITS) {
         if (A) {
             ctx.unsupported = true;
@@ -401,9 +435,9 @@ bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx)
 
 template void launch_fit<FLR_Q>(int, int, int, int, int, int, const float*, const float*, float*,
                                 double*, double*, float*, int, double, double, const Taps&,
-                                LaunchCtx&, const float*, float);
+                                LaunchCtx&, const float*, float, bool);
 template void launch_apply<FLR_Q>(int, int, int, int, int, int, const float*, int, const float*,
-                                  float*, LaunchCtx&, const float*, const float*);
+                                  float*, LaunchCtx&, const float*, const float*, bool);
 template bool launch_fused<FLR_Q>(const FusedLaunch&, LaunchCtx&);
 template <int Q>
 bool apply_mod_supported()

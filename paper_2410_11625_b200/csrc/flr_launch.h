@@ -87,7 +87,8 @@ struct LaunchCtx {
 template <int Q>
 void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, const float* Y,
                 float* raw, double* mom, double* hb, float* models, int mstride, double ea,
-                double em, const Taps& taps, LaunchCtx& ctx, const float* A = nullptr, float afloor = 0.f);
+                double em, const Taps& taps, LaunchCtx& ctx, const float* A = nullptr, float afloor = 0.f,
+                bool hg = false);
 
 // K4 with the fastest kernel the shape allows
 // A (optional): albedo [n][3][H][W]; out = A * I + Dl (Dl optional direct light), fused into
@@ -95,7 +96,23 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
 template <int Q>
 void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* models, int mstride,
                   const float* G, float* out, LaunchCtx& ctx, const float* A = nullptr,
-                  const float* Dl = nullptr);
+                  const float* Dl = nullptr, bool hg = false);
+
+// hg (half guides): G points to IEEE binary16 planes; only the warp-specialised TMA kernels
+// read them, so the shape must satisfy half_guides_ok() (the API checks before launching)
+inline bool half_guides_fit_ok(int D, int W, const void* G, const void* Y)
+{
+    return (D == 4 || D == 8 || D == 16) && aligned(G, 16) && W % 8 == 0 && vec_ok(Y, W);
+}
+inline bool half_guides_apply_ok(int D, int W, const void* models, const void* G, const void* out)
+{
+    return D % 8 == 0 && aligned(models, 16) && aligned(G, 16) && W % 8 == 0 && vec_ok(out, W);
+}
+// fp16 planes [planes][H][W], box {bx, 1, bz}
+inline bool make_tmap_planes_f16(CUtensorMap* m, const void* base, int W, int H, int planes, int bx, int bz)
+{
+    return make_tmap_3d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W, H, W, planes, bx, 1, bz);
+}
 
 // shapes for which the modulated (albedo) protocol runs fused into the TMA kernels
 inline bool fit_mod_fused(int D, int W, const void* G, const void* Y, const void* A)
@@ -130,10 +147,10 @@ bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx);
 #define FLR_DECLARE_Q(Q)                                                                          \
     extern template void launch_fit<Q>(int, int, int, int, int, int, const float*, const float*,  \
                                        float*, double*, double*, float*, int, double, double,     \
-                                       const Taps&, LaunchCtx&, const float*, float);             \
+                                       const Taps&, LaunchCtx&, const float*, float, bool);       \
     extern template void launch_apply<Q>(int, int, int, int, int, int, const float*, int,         \
                                          const float*, float*, LaunchCtx&, const float*,          \
-                                         const float*);                                           \
+                                         const float*, bool);                                     \
     extern template bool launch_fused<Q>(const FusedLaunch&, LaunchCtx&);                      \
     extern template bool apply_mod_supported<Q>();
 FLR_DECLARE_Q(1) FLR_DECLARE_Q(2) FLR_DECLARE_Q(3) FLR_DECLARE_Q(4) FLR_DECLARE_Q(5)

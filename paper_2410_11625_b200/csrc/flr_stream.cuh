@@ -110,15 +110,17 @@ struct FitArgs {
     float afloor;    // albedo floor of the demodulation (modulated fit only)
 };
 
-template <int Q, int D, bool MOD = false>
+// HG: the guide planes are IEEE binary16 (half the stage bytes of the guides)
+template <int Q, int D, bool MOD = false, bool HG = false>
 __device__ __forceinline__ void fit_issue_row(const FitArgs& a, int f, int by, int sg, int rr, float* dst,
                                               uint64_t* bar, uint64_t pol_g, uint64_t pol_y)
 {
-    mbar_arrive_expect_tx(bar, (Q + 3 + (MOD ? 3 : 0)) * kSeg * 4);
+    constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats of stage per guide plane
+    mbar_arrive_expect_tx(bar, (Q * GF + (3 + (MOD ? 3 : 0)) * kSeg) * 4);
     const int x = sg * kSeg, y = by * D + rr;
     tma_load_3d(dst, &a.tg, x, y, f * Q, bar, pol_g);
-    tma_load_3d(dst + Q * kSeg, &a.ty, x, y, f * 3, bar, pol_y);
-    if (MOD) tma_load_3d(dst + (Q + 3) * kSeg, &a.ta, x, y, f * 3, bar, pol_y);
+    tma_load_3d(dst + Q * GF, &a.ty, x, y, f * 3, bar, pol_y);
+    if (MOD) tma_load_3d(dst + Q * GF + 3 * kSeg, &a.ta, x, y, f * 3, bar, pol_y);
 }
 
 // packed-pair layout of the FIT accumulators: d is paired over planes (2p, 2p+1)
@@ -452,15 +454,16 @@ __device__ __forceinline__ void apply_issue_models(const ApplyArgs& a, const App
 }
 
 // guide row y of an APPLY item (lane 0)
-template <int Q, bool MOD = false>
+template <int Q, bool MOD = false, bool HG = false>
 __device__ __forceinline__ void apply_issue_row(const ApplyArgs& a, const ApplyGeom& g, int f, int y, float* dst,
                                                 uint64_t* bar, uint64_t pol_g)
 {
-    mbar_arrive_expect_tx(bar, (Q + (MOD ? (a.has_direct ? 6 : 3) : 0)) * kSeg * 4);
+    constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats of stage per guide plane
+    mbar_arrive_expect_tx(bar, (Q * GF + (MOD ? (a.has_direct ? 6 : 3) : 0) * kSeg) * 4);
     tma_load_3d(dst, &a.tg, g.xs, y, f * Q, bar, pol_g);
     if (MOD) {  // remodulation planes: albedo, then the direct light
-        tma_load_3d(dst + Q * kSeg, &a.ta, g.xs, y, f * 3, bar, pol_g);
-        if (a.has_direct) tma_load_3d(dst + (Q + 3) * kSeg, &a.td, g.xs, y, f * 3, bar, pol_g);
+        tma_load_3d(dst + Q * GF, &a.ta, g.xs, y, f * 3, bar, pol_g);
+        if (a.has_direct) tma_load_3d(dst + Q * GF + 3 * kSeg, &a.td, g.xs, y, f * 3, bar, pol_g);
     }
 }
 
