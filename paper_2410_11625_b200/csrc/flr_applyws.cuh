@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws
 {
     using C = ApplyWsCfg<Q, MOD, HG>;
     constexpr int GF = C::GF, RO = Q * GF;  // RO: first remodulation plane (floats)
+    if (threadIdx.x == 0) FLR_TL(2, 0);
     using SD = StreamDims<Q>;
     constexpr int NC = C::NC, S = C::S, SM = C::SM, MS = SD::MS;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws
             pre = kr;
         }
         pdl_wait();  // the models come from the previous grid
+        if (lane == 0) FLR_TL(2, 1);
         constexpr unsigned mask = (1u << NC) - 1;
         while (__any_sync(mask, it < nitems)) {
             if (it >= nitems) continue;
@@ -261,6 +263,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws
             }
         }
     }
+    if (threadIdx.x == 0) FLR_TL(2, 2);
 }
 
 }  // namespace flr

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
 {
     using C = FitWsCfg<Q, MOD, HG>;
     using Dm = Dims<Q>;
+    if (threadIdx.x == 0) FLR_TL(0, 0);
     constexpr int NC = C::NC, S = C::S, STG = C::STG, DQ = D / 4;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* stages = reinterpret_cast<float*>(smem_raw);
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     const int per_frame = a.By * a.nseg, nitems = n * per_frame, GW = gridDim.x * NC;
     pdl_wait();  // caller data may come from the previous grid
     pdl_trigger();  // dependents launch only once we are past our own wait
+    if (threadIdx.x == 0) FLR_TL(0, 1);
 
     if (warp == NC) {
         // ---------------- producer: lane c feeds consumer c ----------------
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
             if (lane == 0) red_release_add(&a.done[f * a.By + by], 1);
         }
     }
+    if (threadIdx.x == 0) FLR_TL(0, 2);
 }
 
 }  // namespace flr

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
     double* st = vb + KG::VB;
     uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(smk) + KG::BAR_OFF);
     const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+    if (tid == 0) FLR_TL(1, 0);
     const int bx0 = blockIdx.x * TX, by0 = blockIdx.y * TY, f = blockIdx.z;
 #ifdef FLR_DBG_PHASES
     extern __device__ long long g_flr_phase[];
@@ -92,6 +93,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
     if (!wait_rows) {
         pdl_wait();  // the moment field comes from the previous grid
         pdl_trigger();  // dependents launch only once we are past our own wait
+        if (tid == 0) FLR_TL(1, 1);
     } else {
         pdl_trigger();  // wavefront: wait only for the FIT rows this tile reads (+- R), one thread per row
         const int rr = by0 - R + tid;
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
     __syncthreads();
     if (tid == 0) g_flr_phase[1000 + 4 * cta_id + 1] = gtimer(), g_flr_phase[1000 + 4 * cta_id + 2] = tsg[NG + 2] - tsg[0];
 #endif
+    if (tid == 0) FLR_TL(1, 2);
     if (signal) {  // publish this tile's models to the APPLY wavefront
         __syncthreads();
         if (tid == 0) red_release_add(&signal[f * gridDim.y + blockIdx.y], 1);

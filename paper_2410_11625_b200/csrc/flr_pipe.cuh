@@ -73,6 +73,17 @@ __device__ __forceinline__ long long gtimer()
     return t;
 }
 
+// Optional CTA timeline (tools/t_timeline.cu, -DFLR_TIMELINE): globaltimer stamps per CTA
+// of the three default kernels, [kernel][cta][slot] with slot 0 = entry, 1 = past the
+// grid-dependency wait, 2 = exit.  Compiled out of the library.
+#ifdef FLR_TIMELINE
+__device__ long long g_flr_tl[3 * 1024 * 4];  // single-TU tools only (no -rdc)
+#define FLR_TL(k, slot) \
+    (g_flr_tl[((k) * 1024 + blockIdx.x + blockIdx.y * gridDim.x) * 4 + (slot)] = gtimer())
+#else
+#define FLR_TL(k, slot) ((void)0)
+#endif
+
 // ---- L2 cache policies --------------------------------------------------------
 __device__ __forceinline__ uint64_t policy_evict_first()
 {
