@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every step from Python")
     ap.add_argument("--check", action="store_true", help="parity-check one frame against the oracle")
+    ap.add_argument("--modulated", action="store_true",
+                    help="the paper's albedo protocol (flr_denoise_modulated: demodulate, denoise, remodulate, "
+                         "add direct light; SURVEY f1) on the c2 shape")
     ap.add_argument("--guides", choices=["f32", "f16"], default="f32",
                     help="guide plane precision (f16: the fp16 guide network's output, SURVEY f2)")
     return ap.parse_args()
@@ -83,6 +86,8 @@ def min_bytes_per_frame(cfg):
     Q, W, H, U, gb = cfg["Q"], cfg["W"], cfg["H"], cfg["upsample"], cfg.get("gbytes", 4)
     lo = W * H
     hi = lo * U * U
+    if cfg.get("modulated"):  # guides, radiance, albedo, direct read once; output written once
+        return (Q * gb + 4 * 3 * 4) * lo
     if U == 1:
         return (Q * gb + (3 + 3) * 4) * lo
     return (Q * gb + 3 * 4) * lo + Q * gb * hi + 3 * 4 * hi
@@ -96,7 +101,16 @@ def _apply_bytes(c):  # Q guide planes read + 3 output planes written once
     return (c["Q"] * c.get("gbytes", 4) + 3 * 4) * out_pixels(c)
 
 
+def _fit_mod_bytes(c):  # + 3 albedo planes
+    return _fit_bytes(c) + 3 * 4 * c["W"] * c["H"]
+
+
+def _apply_mod_bytes(c):  # + 3 albedo and 3 direct-light planes
+    return _apply_bytes(c) + 6 * 4 * out_pixels(c)
+
+
 KERNEL_BYTES = {
+    "k_fit_ws_mod": _fit_mod_bytes, "k_apply_ws_mod": _apply_mod_bytes,
     # algorithmic bytes per frame of each launch: the full-resolution planes it must read + write
     "k_fit_moments": _fit_bytes, "k_fit_stream": _fit_bytes, "k_fit_ldg": _fit_bytes, "k_fit_ws": _fit_bytes,
     "k_fit_ws_f16": _fit_bytes,
@@ -327,9 +341,15 @@ def run_flr(args, cfg, rank, world, local_rank):
     from paper_2410_11625_b200 import dist as fd
 
     seeds = fd.frame_seeds(rank, world, pool * F)
-    gl, yl, gh = [], [], []
+    gl, yl, gh, al, dl = [], [], [], [], []
     for i in range(pool):
-        if U == 1:
+        if args.modulated:  # the renderer's outputs: modulated radiance, albedo, direct light
+            fr = [synth.modulated_frame(W, H, Q=Q, seed=seeds[i * F + j], device=dev) for j in range(F)]
+            gl.append(torch.stack([t[0] for t in fr]).contiguous())
+            yl.append(torch.stack([t[1] for t in fr]).contiguous())
+            al.append(torch.stack([t[2] for t in fr]).contiguous())
+            dl.append(torch.stack([t[3] for t in fr]).contiguous())
+        elif U == 1:
             g, y = synth.batch(F, W, H, Q=Q, seed0=seeds[i * F], device=dev)
             gl.append(g)
             yl.append(y)
@@ -347,6 +367,8 @@ def run_flr(args, cfg, rank, world, local_rank):
 
     def call(i, trace=None):
         k = i % pool
+        if args.modulated:
+            return den.modulated(gl[k], yl[k], al[k], dl[k], out=outs[i % 2], trace=trace)
         return den(gl[k], yl[k], gh[k] if U > 1 else None, out=outs[i % 2], trace=trace)
 
     # ---- launch count + optional parity check
@@ -362,7 +384,9 @@ def run_flr(args, cfg, rank, world, local_rank):
         o = call(0).cpu().numpy()
         g0 = gl[0].float().cpu().numpy()
         y0 = yl[0].cpu().numpy()
-        if U == 1:
+        if args.modulated:
+            ref = oracle.denoise_modulated(g0, y0, al[0].cpu().numpy(), dl[0].cpu().numpy(), D=D, sigma=sigma, R=R)
+        elif U == 1:
             ref = oracle.denoise(g0, y0, D=D, sigma=sigma, R=R)
         else:
             ref = oracle.denoise_upsample(g0, y0, gh[0].float().cpu().numpy(), D_fit=D, U=U, sigma=sigma, R=R)
@@ -471,7 +495,13 @@ def run_flr(args, cfg, rank, world, local_rank):
         h_out = den.out.cpu().pin_memory()
         d_g, d_y = torch.empty_like(gl[0]), torch.empty_like(yl[0])
         d_gh = torch.empty_like(gh[0]) if U > 1 else None
+        h_a = [al[k].cpu().pin_memory() for k in range(hp)] if args.modulated else None
+        h_dl = [dl[k].cpu().pin_memory() for k in range(hp)] if args.modulated else None
+        d_a = torch.empty_like(al[0]) if args.modulated else None
+        d_dl = torch.empty_like(dl[0]) if args.modulated else None
         h2d = sum(t.numel() * t.element_size() for t in (d_g, d_y)) + (d_gh.numel() * d_gh.element_size() if U > 1 else 0)
+        if args.modulated:
+            h2d += (d_a.numel() + d_dl.numel()) * 4
         d2h = h_out.numel() * 4
 
         def e2e_step(i):
@@ -480,7 +510,12 @@ def run_flr(args, cfg, rank, world, local_rank):
             d_y.copy_(h_y[k], non_blocking=True)
             if U > 1:
                 d_gh.copy_(h_gh[k], non_blocking=True)
-            o = den(d_g, d_y, d_gh)
+            if args.modulated:
+                d_a.copy_(h_a[k], non_blocking=True)
+                d_dl.copy_(h_dl[k], non_blocking=True)
+                o = den.modulated(d_g, d_y, d_a, d_dl)
+            else:
+                o = den(d_g, d_y, d_gh)
             h_out.copy_(o, non_blocking=True)
 
         for i in range(3):
@@ -559,7 +594,7 @@ def run_flr(args, cfg, rank, world, local_rank):
                    "pool_frames": pool, "l2": f"rotating pool of {pool} distinct steps "
                    f"({pool * F * frame_in_bytes / 1e6:.0f} MB > 126 MB L2)", "graphs": use_graph,
                    "parallelism": f"frame-sharded dp{world}", "variant": args.variant,
-                   "guides": args.guides,
+                   "guides": args.guides, "modulated": bool(args.modulated),
                    "numerics": "fp32 streams, fp64 block blur+solve"
                                + ("; fp16 guide planes widened exactly to fp32 on load" if half else "")},
         "roofline": roof, "step_roofline": step_roof,
@@ -579,6 +614,11 @@ def main():
     args = parse()
     cfg = dict(CONFIGS[args.config])
     cfg["gbytes"] = 2 if args.guides == "f16" else 4
+    if args.modulated:
+        if args.config != "c2" or args.guides != "f32":
+            sys.exit("--modulated runs on the c2 shape with fp32 guides")
+        cfg["modulated"] = True
+        cfg["workload"] = "C2 albedo protocol: demodulate, 1080p Q=8 FLR, remodulate + direct light (SURVEY f1)"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

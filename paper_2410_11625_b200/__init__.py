@@ -332,6 +332,22 @@ class Denoiser:
         self.out = torch.empty((n, 3, H * upsample, W * upsample), dtype=torch.float32, device=device)
         self._L = lib()
 
+    def modulated(self, guides, radiance_mod, albedo, direct=None, albedo_floor=1e-3, out=None, stream=None,
+                  trace=None):
+        """The albedo protocol (flr_denoise_modulated) on this shape: one C-ABI call."""
+        torch = _torch()
+        out = self.out if out is None else out
+        s = ctypes.c_void_p(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+        ws = self.workspace
+        tr = ctypes.byref(trace) if trace is not None else None
+        st = self._L.flr_denoise_modulated_traced(self.n, self.Q, self.W, self.H, guides.data_ptr(),
+                                                  radiance_mod.data_ptr(), albedo.data_ptr(),
+                                                  direct.data_ptr() if direct is not None else None,
+                                                  float(albedo_floor), ctypes.byref(self.params), out.data_ptr(),
+                                                  ws.data_ptr(), ws.numel(), s, tr)
+        _check(st, "flr_denoise_modulated_traced")
+        return out
+
     def __call__(self, guides, radiance, guides_hi=None, out=None, stream=None, trace=None):
         """One C-ABI call; `trace` is an optional EventTrace (per-launch CUDA events)."""
         torch = _torch()

@@ -16,8 +16,14 @@
 
 namespace flr {
 
-constexpr int kApplyWsNC = 7;  // consumer warps (+1 producer = 8 warps, 255-register cap)
-constexpr int kApplyWsS = 4;   // guide-row stages per consumer
+#ifndef FLR_APPLYWS_NC
+#define FLR_APPLYWS_NC 7
+#endif
+#ifndef FLR_APPLYWS_S
+#define FLR_APPLYWS_S 4
+#endif
+constexpr int kApplyWsNC = FLR_APPLYWS_NC;  // consumer warps (+1 producer = 8 warps, 255-register cap)
+constexpr int kApplyWsS = FLR_APPLYWS_S;  // guide-row stages per consumer
 constexpr int kApplyWsM = 2;   // model stages per consumer
 
 template <int Q, bool MOD = false, bool HG = false>

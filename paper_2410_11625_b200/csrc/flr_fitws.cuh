@@ -19,7 +19,10 @@
 
 namespace flr {
 
-constexpr int kFitWsNC = 7;  // consumer warps (+1 producer = 8 warps: 2 per SMSP keeps the 255-register cap)
+#ifndef FLR_FITWS_NC
+#define FLR_FITWS_NC 7
+#endif
+constexpr int kFitWsNC = FLR_FITWS_NC;  // consumer warps (+1 producer = 8 warps: 2 per SMSP keeps the 255-register cap)
 #ifndef FLR_FITWS_S
 #define FLR_FITWS_S 4
 #endif
