@@ -93,10 +93,19 @@ typedef struct {
     double eps_add;   /* additive regulariser epsilon >= 0; default 1e-5 */
     double eps_mul;   /* multiplicative regulariser epsilon^ in [0,1); default 1e-4 */
     int32_t solver;   /* flr_solver; default FLR_SOLVER_APPENDIX */
+    int32_t flags;    /* FLR_FLAG_* bits; default 0 */
 } flr_params;
 
+/* The call's inputs (guides, radiance, albedo, direct light) were complete before the kernel
+ * that precedes the call on `stream` began (e.g. written by a copy, or by an earlier call's
+ * caller): the moment kernel then starts streaming them while that kernel drains, instead of
+ * waiting for it (programmatic dependent launch).  Its dependents still launch only after
+ * the preceding kernel completed, so the library's own workspace is never raced.  Without
+ * the flag every call waits for the preceding kernel before reading its inputs. */
+#define FLR_FLAG_INPUTS_READY 1
+
 /* Fill *p with the defaults: block 8, upsample 1, radius 0 (auto), variant AUTO,
- * sigma 10, eps_add 1e-5, eps_mul 1e-4, solver APPENDIX.  No-op on NULL. */
+ * sigma 10, eps_add 1e-5, eps_mul 1e-4, solver APPENDIX, flags 0.  No-op on NULL. */
 void flr_default_params(flr_params* p);
 
 /* Static human-readable name of a status; never NULL. */

@@ -31,6 +31,7 @@ VARIANT_STAGED = 1
 VARIANT_FUSED = 2
 SOLVER_APPENDIX = 0  # the paper's normalised solve
 SOLVER_TIKHONOV = 1  # Eq. tikhonov, Fig. 3 semantics; eps_add is its epsilon
+FLAG_INPUTS_READY = 1  # inputs complete before the preceding kernel began (streaming loops)
 
 
 class EventTrace(ctypes.Structure):
@@ -58,13 +59,13 @@ class Params(ctypes.Structure):
     """Mirror of flr_params (include/flr.h)."""
     _fields_ = [("block", ctypes.c_int32), ("upsample", ctypes.c_int32), ("radius", ctypes.c_int32),
                 ("variant", ctypes.c_int32), ("sigma", ctypes.c_double), ("eps_add", ctypes.c_double),
-                ("eps_mul", ctypes.c_double), ("solver", ctypes.c_int32)]
+                ("eps_mul", ctypes.c_double), ("solver", ctypes.c_int32), ("flags", ctypes.c_int32)]
 
     @classmethod
     def make(cls, block=8, upsample=1, sigma=10.0, radius=0, eps_add=1e-5, eps_mul=1e-4,
-             variant=VARIANT_AUTO, solver=0):
+             variant=VARIANT_AUTO, solver=0, flags=0):
         return cls(int(block), int(upsample), int(radius), int(variant), float(sigma),
-                   float(eps_add), float(eps_mul), int(solver))
+                   float(eps_add), float(eps_mul), int(solver), int(flags))
 
 
 def lib_path() -> str:
@@ -322,10 +323,10 @@ class Denoiser:
     Holds the ctypes argument objects so a call is one C-ABI call with no allocation."""
 
     def __init__(self, n, Q, W, H, device="cuda", block=8, upsample=1, sigma=10.0, radius=0,
-                 eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX):
+                 eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, flags=0):
         torch = _torch()
         self.n, self.Q, self.W, self.H, self.U = n, Q, W, H, upsample
-        self.params = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver)
+        self.params = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver, flags)
         nbytes = workspace_size(n, Q, W, H, block=block, upsample=upsample, sigma=sigma, radius=radius,
                                 eps_add=eps_add, eps_mul=eps_mul, variant=variant)
         self.workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)

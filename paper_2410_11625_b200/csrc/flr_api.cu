@@ -30,6 +30,7 @@ flr_status check_params(const flr_params* p)
     if (!(p->eps_mul >= 0.0) || !(p->eps_mul < 1.0)) return FLR_ERR_INVALID_VALUE;
     if (p->radius < 0) return FLR_ERR_INVALID_VALUE;
     if (p->solver != FLR_SOLVER_APPENDIX && p->solver != FLR_SOLVER_TIKHONOV) return FLR_ERR_INVALID_VALUE;
+    if (p->flags & ~FLR_FLAG_INPUTS_READY) return FLR_ERR_INVALID_VALUE;
     if (p->variant != FLR_VARIANT_AUTO && p->variant != FLR_VARIANT_STAGED && p->variant != FLR_VARIANT_FUSED)
         return FLR_ERR_UNSUPPORTED;
     return FLR_OK;
@@ -158,6 +159,7 @@ flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, co
     // B200 (the per-item release and the per-call flag reset cost more than the overlap)
     static const bool wave = std::getenv("FLR_WAVE") != nullptr;
     ctx.wave_flags = wave ? (int*)(base + L.flags) : nullptr;
+    ctx.early = (p->flags & FLR_FLAG_INPUTS_READY) && !wave;
     FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, G, Y, (float*)(base + L.raw),
                                       (double*)(base + L.mom), (double*)(base + L.hb), models,
                                       mstride, p->eps_add, solver_eps_mul(p), taps, ctx, nullptr, 0.f, hg)));
@@ -210,6 +212,7 @@ void flr_default_params(flr_params* p)
     p->eps_add = 1e-5;
     p->eps_mul = 1e-4;
     p->solver = FLR_SOLVER_APPENDIX;
+    p->flags = 0;
 }
 
 const char* flr_status_string(flr_status s)
@@ -443,6 +446,7 @@ flr_status flr_denoise_modulated_traced(int32_t n, int32_t Q, int32_t W, int32_t
         const double sblk = p->sigma / (double)D;
         const Taps taps = make_taps(sblk, effective_radius(p));
         char* base = (char*)workspace;
+        ctx.early = (p->flags & FLR_FLAG_INPUTS_READY) != 0;
         FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, guides, radiance_mod, (float*)(base + L.raw),
                                           (double*)(base + L.mom), (double*)(base + L.hb), models, ms,
                                           p->eps_add, solver_eps_mul(p), taps, ctx, albedo, albedo_floor)));

@@ -73,7 +73,10 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws
     // waits (griddepcontrol.wait), and only after it has queued the first guide rows: the
     // guides are inputs of the call, complete before the fit grid got past its own wait
     // (every grid of the chain triggers its dependents only after its wait).
-    pdl_trigger();
+    // Dependents (normally the next call's moment grid) launch only once the models' grid has
+    // completed (the producer's lane 0 triggers after its wait): a following moment grid that
+    // streams before its own wait (FLR_FLAG_INPUTS_READY) then cannot overwrite the moment
+    // field K2 is still reading.
 
     auto geom = [&](int it, int& f) {
         f = it / per_frame;
@@ -115,6 +118,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws
             pre = kr;
         }
         pdl_wait();  // the models come from the previous grid
+        if (lane == 0) pdl_trigger();
         if (lane == 0) FLR_TL(2, 1);
         constexpr unsigned mask = (1u << NC) - 1;
         while (__any_sync(mask, it < nitems)) {

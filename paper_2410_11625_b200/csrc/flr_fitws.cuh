@@ -171,8 +171,15 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     }
     __syncthreads();
     const int per_frame = a.By * a.nseg, nitems = n * per_frame, GW = gridDim.x * NC;
-    pdl_wait();  // caller data may come from the previous grid
-    pdl_trigger();  // dependents launch only once we are past our own wait
+    // Default: the inputs may come from the previous grid, so wait for it before streaming.
+    // Early (inputs ready before the previous grid began): stream at once, and run the wait
+    // (+ trigger) once this CTA has issued its last row, so the dependents -- K2, which writes
+    // the models the previous call's apply may still be reading -- launch only after the
+    // previous grid completed.
+    if (!a.early) {
+        pdl_wait();  // caller data may come from the previous grid
+        pdl_trigger();  // dependents launch only once we are past our own wait
+    }
     if (threadIdx.x == 0) FLR_TL(0, 1);
 
     if (warp == NC) {
@@ -207,6 +214,10 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
                     decode();
                 }
             }
+        }
+        if (a.early && lane == 0) {
+            pdl_wait();
+            pdl_trigger();
         }
         return;
     }

@@ -74,7 +74,7 @@ static int num_sms()
 // returns true when the TMA-ring kernel ran with `done` row counters (K2 may then wait per row)
 template <int Q, int D>
 static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
-                      int* done, cudaStream_t s, const float* A, float afloor, bool hg)
+                      int* done, cudaStream_t s, const float* A, float afloor, bool hg, bool early)
 {
     if (hg) {  // fp16 guide planes: the warp-specialised kernel with a half-width guide stage
         FitArgs a;
@@ -83,6 +83,7 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
             return false;
         a.mom = mom;
         a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
+        a.early = early;
         using C = FitWsCfg<Q, false, true>;
         const int grid = min(num_sms(), cdiv(n * By * a.nseg, C::NC));
         set_smem(k_fit_ws<Q, D, false, true>, C::SMEM);
@@ -99,6 +100,7 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
         a.done = nullptr;
         a.gpol = 0;
         a.afloor = afloor;
+        a.early = early;
         using C = FitWsCfg<Q, true>;
         const int grid = min(num_sms(), cdiv(n * By * a.nseg, C::NC));
         set_smem(k_fit_ws<Q, D, true>, C::SMEM);
@@ -119,6 +121,7 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
         a.mom = mom;
         a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
         a.done = done;
+        a.early = early && !std::getenv("FLR_FIT_RING");
         static const int gpol = std::getenv("FLR_FIT_GPOL") ? std::atoi(std::getenv("FLR_FIT_GPOL")) : 0;
         a.gpol = gpol;
 
@@ -165,9 +168,9 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
         ctx.before(hg ? "k_fit_ws_f16" : A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : std::getenv("FLR_FIT_RING") ? "k_fit_stream" : "k_fit_ws");
-        if (D == 4) fit_signals = launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg);
-        else if (D == 8) fit_signals = launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg);
-        else fit_signals = launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg);
+        if (D == 4) fit_signals = launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg, ctx.early && !fit_done);
+        else if (D == 8) fit_signals = launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg, ctx.early && !fit_done);
+        else fit_signals = launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, fit_done, s, A, afloor, hg, ctx.early && !fit_done);
     } else {
         ctx.before("k_moments_small");
         k_moments_small<Q><<<dim3(cdiv(Bx, 128), By, n), 128, 0, s>>>(W, H, Bx, By, D, G, Y, raw);

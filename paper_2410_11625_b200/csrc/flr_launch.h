@@ -57,6 +57,7 @@ struct LaunchCtx {
     int recorded = 0;
     bool capturing = false;   // stream capture: events become graph event-record nodes
     bool unsupported = false; // set by launchers compiled out of a dev build (FLR_STUB)
+    bool early = false;       // FLR_FLAG_INPUTS_READY: the moment grid streams before its grid wait
     // row wavefront across the K1 -> K2 -> K3 grids (flags zeroed per call): K2 tiles wait
     // on per-row FIT counters, APPLY items on per-tile-row K2 counters, instead of on the
     // completion of the whole previous grid (griddepcontrol.wait)

@@ -108,6 +108,8 @@ struct FitArgs {
     int gpol;        // L2 policy code (policy_by_code) of the guide reads
     CUtensorMap ta;  // albedo [n*3][H][W], box {128, 1, 3} (modulated fit only)
     float afloor;    // albedo floor of the demodulation (modulated fit only)
+    int early;       // inputs ready (FLR_FLAG_INPUTS_READY): stream before the grid-dependency
+                     // wait, which then only gates this grid's dependents (see k_fit_ws)
 };
 
 // HG: the guide planes are IEEE binary16 (half the stage bytes of the guides)
