@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared(header):
     src = open(header).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(flr_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(flr_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -27,7 +27,8 @@ def L():
 
 def test_exports_every_declared_symbol(L):
     names = _declared(os.path.join(ROOT, "include", "flr.h"))
-    assert {"flr_fit", "flr_apply", "flr_denoise", "flr_denoise_upsample"} <= set(names)
+    assert {"flr_fit", "flr_apply", "flr_denoise", "flr_denoise_upsample", "flr_denoise_modulated",
+            "flr_fit_f16", "flr_denoise_f16", "flr_denoise_upsample_f16"} <= set(names)
     for n in names:
         assert hasattr(L, n), n
 
@@ -141,3 +142,47 @@ def test_solver_field_validated(L):
     for s, ok in ((0, True), (1, True), (2, False), (-1, False)):
         p.solver = s
         assert (L.flr_effective_radius(ctypes.byref(p)) >= 0) == ok
+
+
+def test_flags_field_validated(L):
+    p = flr.Params()
+    L.flr_default_params(ctypes.byref(p))
+    assert p.flags == 0
+    p.flags = flr.FLAG_INPUTS_READY
+    assert L.flr_effective_radius(ctypes.byref(p)) >= 0
+    p.flags = 2  # unknown bit
+    assert L.flr_effective_radius(ctypes.byref(p)) == -1
+
+
+def test_modulated_argument_checks(L):
+    """flr_denoise_modulated validates before launching (no GPU touched)."""
+    p = _p()
+    big = 1 << 40
+    f = ctypes.c_float
+    # NULL albedo, non-positive / NaN floor -> INVALID_VALUE
+    assert L.flr_denoise_modulated(1, 8, 64, 64, FAKE, FAKE, None, None, f(1e-3), ctypes.byref(p), FAKE, FAKE,
+                                   big, None) == 1
+    assert L.flr_denoise_modulated(1, 8, 64, 64, FAKE, FAKE, FAKE, None, f(0.0), ctypes.byref(p), FAKE, FAKE,
+                                   big, None) == 1
+    assert L.flr_denoise_modulated(1, 8, 64, 64, FAKE, FAKE, FAKE, None, f(float("nan")), ctypes.byref(p), FAKE,
+                                   FAKE, big, None) == 1
+    # upsample must be 1; misaligned direct light
+    pu = _p(upsample=2, block=4)
+    assert L.flr_denoise_modulated(1, 8, 64, 64, FAKE, FAKE, FAKE, None, f(1e-3), ctypes.byref(pu), FAKE, FAKE,
+                                   big, None) == 1
+    assert L.flr_denoise_modulated(1, 8, 64, 64, FAKE, FAKE, FAKE, ctypes.c_void_p(0x7F0000000002), f(1e-3),
+                                   ctypes.byref(p), FAKE, FAKE, big, None) == 3
+
+
+def test_half_guide_entry_points_reject_unsupported_shapes(L):
+    """The fp16-guide entry points run only the TMA kernels: W % 8, block 4/8/16 (fit) and
+    output blocks of a multiple of 8 (apply); anything else is UNSUPPORTED before launch."""
+    big = 1 << 40
+    p = _p()
+    assert L.flr_fit_f16(1, 8, 68, 64, FAKE, FAKE, ctypes.byref(p), FAKE, FAKE, big, None) == 5  # W % 8
+    assert L.flr_fit_f16(1, 8, 64, 64, FAKE, FAKE, ctypes.byref(_p(block=2)), FAKE, FAKE, big, None) == 5
+    assert L.flr_denoise_f16(1, 8, 64, 64, FAKE, FAKE, ctypes.byref(_p(block=4)), FAKE, FAKE, big, None) == 5
+    assert L.flr_denoise_f16(1, 8, 64, 64, FAKE, FAKE, ctypes.byref(_p(variant=flr.VARIANT_FUSED)), FAKE, FAKE,
+                             big, None) == 5
+    assert L.flr_denoise_upsample_f16(1, 8, 32, 32, FAKE, FAKE, 64, 64, FAKE, ctypes.byref(_p(block=2, upsample=2)),
+                                      FAKE, FAKE, big, None) == 5
