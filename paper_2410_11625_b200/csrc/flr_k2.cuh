@@ -196,11 +196,23 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
     }
 #endif
     const int nbx = min(TX, Bx - bx0);
+    static_assert(MS % 4 == 0, "padded models are whole float4s");
+#ifndef FLR_K2_SCALAR_STORE
+    {  // the tile's rows are contiguous runs of nbx models (16-byte aligned): float4 stores
+        const int nrow = min(TY, By - by0), q = nbx * (MS / 4);
+        for (int i = tid; i < nrow * q; i += kK2Threads) {
+            const int r = i / q, j = i - r * q;
+            reinterpret_cast<float4*>(models + ((size_t)(f * By + by0 + r) * Bx + bx0) * MS)[j] =
+                reinterpret_cast<const float4*>(mstage + r * TX * MS)[j];
+        }
+    }
+#else
     for (int r = 0; r < TY && by0 + r < By; ++r) {  // one contiguous run of nbx models per row
         float* dst = models + ((size_t)(f * By + by0 + r) * Bx + bx0) * MS;
         const float* src = mstage + r * TX * MS;
         for (int i = tid; i < nbx * MS; i += kK2Threads) dst[i] = src[i];
     }
+#endif
 #ifdef FLR_DBG_PHASES
     __syncthreads();
     if (tid == 0) g_flr_phase[1000 + 4 * cta_id + 1] = gtimer(), g_flr_phase[1000 + 4 * cta_id + 2] = tsg[NG + 2] - tsg[0];
