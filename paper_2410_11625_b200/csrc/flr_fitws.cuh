@@ -27,13 +27,20 @@ constexpr int kFitWsNC = FLR_FITWS_NC;  // consumer warps (+1 producer = 8 warps
 #define FLR_FITWS_S 4
 #endif
 constexpr int kFitWsS = FLR_FITWS_S;  // ring stages per consumer
+#ifndef FLR_FIT_SEG
+#define FLR_FIT_SEG 128
+#endif
+// segment width of a FIT item in pixels: 128 (4 pixels per lane) or 64 (2 per lane: half the
+// bytes per item, for a shorter grid tail; give it twice the stages)
+constexpr int kFS = FLR_FIT_SEG, kPPL = kFS / 32, kNH = kPPL / 2;
+static_assert(kFS == 128 || kFS == 64, "fit segment: 64 or 128 pixels");
 
 template <int Q, bool MOD = false, bool HG = false>
 struct FitWsCfg {
     // floats per stage (one pixel row): Q guide planes (fp32, or fp16 when HG), 3 radiance
     // planes (+ 3 albedo planes)
-    static constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats per guide plane
-    static constexpr int STG = Q * GF + (3 + (MOD ? 3 : 0)) * kSeg;
+    static constexpr int GF = HG ? kFS / 2 : kFS;  // floats per guide plane
+    static constexpr int STG = Q * GF + (3 + (MOD ? 3 : 0)) * kFS;
     // as many stages (<= kFitWsS) as fit in 227 KB with 7 consumers
     static constexpr int fit_stages(int s)
     {
@@ -103,7 +110,7 @@ __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], c
         const float* st = ring + (k % S) * STG;
 #pragma unroll
         for (int j = 0; j < Q; ++j)
-            cs[j] = HG ? __half2float(reinterpret_cast<const __half*>(st + j * GF)[lb0]) : st[j * kSeg + lb0];
+            cs[j] = HG ? __half2float(reinterpret_cast<const __half*>(st + j * GF)[lb0]) : st[j * kFS + lb0];
     }
 #pragma unroll 1  // keep the row body resident in the instruction cache
     for (int rr = 0; rr < rows; ++rr, ++k) {
@@ -111,23 +118,23 @@ __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], c
         mbar_wait(&full[slot], (k / S) & 1);
         const float* st = ring + slot * STG;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kNH; ++h) {
             f2 d[Q], y[3];
 #pragma unroll
             for (int j = 0; j < Q; ++j) {
                 if (HG) {  // fp16 guide pair -> fp32 (exact)
-                    const float2 v = __half22float2(reinterpret_cast<const __half2*>(st + j * GF)[2 * lane + h]);
+                    const float2 v = __half22float2(reinterpret_cast<const __half2*>(st + j * GF)[kNH * lane + h]);
                     d[j] = pk2(v.x, v.y);
                 } else {
-                    d[j] = reinterpret_cast<const f2*>(st + j * kSeg)[2 * lane + h];
+                    d[j] = reinterpret_cast<const f2*>(st + j * kFS)[kNH * lane + h];
                 }
             }
 #pragma unroll
-            for (int c = 0; c < 3; ++c) y[c] = reinterpret_cast<const f2*>(st + RO + c * kSeg)[2 * lane + h];
+            for (int c = 0; c < 3; ++c) y[c] = reinterpret_cast<const f2*>(st + RO + c * kFS)[kNH * lane + h];
             if (MOD) {  // demodulation y = radiance / max(albedo, floor) (R20)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const f2 al = reinterpret_cast<const f2*>(st + RO + (3 + c) * kSeg)[2 * lane + h];
+                    const f2 al = reinterpret_cast<const f2*>(st + RO + (3 + c) * kFS)[kNH * lane + h];
                     y[c] = pk2(lo2(y[c]) * __frcp_rn(fmaxf(lo2(al), afloor)),
                                hi2(y[c]) * __frcp_rn(fmaxf(hi2(al), afloor)));
                 }
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     using C = FitWsCfg<Q, MOD, HG>;
     using Dm = Dims<Q>;
     if (threadIdx.x == 0) FLR_TL(0, 0);
-    constexpr int NC = C::NC, S = C::S, STG = C::STG, DQ = D / 4;
+    constexpr int NC = C::NC, S = C::S, STG = C::STG, DQ = D / kPPL;  // DQ: lanes per block
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* stages = reinterpret_cast<float*>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF);
@@ -205,7 +212,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
             const int slot = k % S;
             if (it < nitems && (k < S || mbar_test_wait(&empty[c * S + slot], ((k / S) - 1) & 1))) {
                 ws_proxy_fence();
-                fit_issue_row<Q, D, MOD, HG>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
+                fit_issue_row<Q, D, MOD, HG, kFS>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
                                     pg, py);
                 ++k;
                 if (++row == rows) {
@@ -229,11 +236,11 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     for (int it = blockIdx.x * NC + w; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it - f * per_frame, by = rem / a.nseg, sg = rem - by * a.nseg;
         const int rows = min(D, a.H - by * D);
-        const int x0 = sg * kSeg + lane * 4, bx = x0 / D, lb0 = (lane / DQ) * D;
+        const int x0 = sg * kFS + lane * kPPL, bx = x0 / D, lb0 = (lane / DQ) * D;
         float cs[Q];
         FitAccPix<Q> acc;
         acc.zero();
-        if (sg * kSeg + kSeg > a.W)  // segment reaches past the image
+        if (sg * kFS + kFS > a.W)  // segment reaches past the image
             fit_ws_rows<Q, D, true, MOD, HG>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
                                          a.afloor);
         else

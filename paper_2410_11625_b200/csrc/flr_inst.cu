@@ -79,10 +79,10 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
     if (hg) {  // fp16 guide planes: the warp-specialised kernel with a half-width guide stage
         FitArgs a;
         std::memset(&a, 0, sizeof(a));
-        if (!make_tmap_planes_f16(&a.tg, G, W, H, n * Q, kSeg, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kSeg, 3))
+        if (!make_tmap_planes_f16(&a.tg, G, W, H, n * Q, kFS, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3))
             return false;
         a.mom = mom;
-        a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
+        a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kFS);
         a.early = early;
         using C = FitWsCfg<Q, false, true>;
         const int grid = min(num_sms(), cdiv(n * By * a.nseg, C::NC));
@@ -92,11 +92,11 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
     }
     if (A) {  // modulated fit: the warp-specialised kernel with the albedo planes in its ring
         FitArgs a;
-        if (!make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kSeg, 3) ||
-            !make_tmap_planes(&a.ta, A, W, H, n * 3, kSeg, 3))
+        if (!make_tmap_planes(&a.tg, G, W, H, n * Q, kFS, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3) ||
+            !make_tmap_planes(&a.ta, A, W, H, n * 3, kFS, 3))
             return false;
         a.mom = mom;
-        a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
+        a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kFS);
         a.done = nullptr;
         a.gpol = 0;
         a.afloor = afloor;
@@ -116,10 +116,12 @@ static bool launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
         return false;
     }
     FitArgs a;
-    if (vec_ok(G, W) && vec_ok(Y, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q) &&
-        make_tmap_planes(&a.ty, Y, W, H, n * 3, kSeg, 3)) {  // TMA-fed persistent path
+    static const bool ring_env = std::getenv("FLR_FIT_RING") != nullptr;
+    const int sw = ring_env ? kSeg : kFS;  // TMA box width = segment width of the kernel
+    if (vec_ok(G, W) && vec_ok(Y, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, sw, Q) &&
+        make_tmap_planes(&a.ty, Y, W, H, n * 3, sw, 3)) {  // TMA-fed persistent path
         a.mom = mom;
-        a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kSeg);
+        a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, sw);
         a.done = done;
         a.early = early && !std::getenv("FLR_FIT_RING");
         static const int gpol = std::getenv("FLR_FIT_GPOL") ? std::atoi(std::getenv("FLR_FIT_GPOL")) : 0;
@@ -165,6 +167,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     if (fit_done) cudaMemsetAsync(fit_done, 0, sizeof(int) * (size_t)n * (By + cdiv(By, kK2TY)), s);
     ctx.wave_k2 = nullptr;
     bool fit_signals = false;
+    const int fit_nseg = cdiv(W, std::getenv("FLR_FIT_RING") ? kSeg : kFS);  // FIT items per block row
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
         ctx.before(hg ? "k_fit_ws_f16" : A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : std::getenv("FLR_FIT_LDG") ? "k_fit_ldg" : std::getenv("FLR_FIT_RING") ? "k_fit_stream" : "k_fit_ws");
@@ -206,7 +209,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
         ctx.before("k_blur_solve_tile");                                                                    \
         set_smem(k_blur_solve_tile<Q, RR>, KG::SMEM);                                                       \
         launch_pdl(k_blur_solve_tile<Q, RR>, grid, dim3(kK2Threads), KG::SMEM, s, tm, Bx, By, models, ea, em, \
-                   taps, (const int*)(fit_signals ? fit_done : nullptr), cdiv(W, kSeg), k2_done, k2pol);    \
+                   taps, (const int*)(fit_signals ? fit_done : nullptr), fit_nseg, k2_done, k2pol);           \
         k2tile = true;                                                                                      \
         break;                                                                                              \
     }

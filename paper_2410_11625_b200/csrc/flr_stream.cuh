@@ -113,16 +113,17 @@ struct FitArgs {
 };
 
 // HG: the guide planes are IEEE binary16 (half the stage bytes of the guides)
-template <int Q, int D, bool MOD = false, bool HG = false>
+// SW: segment width in pixels (the TMA box width of every plane)
+template <int Q, int D, bool MOD = false, bool HG = false, int SW = kSeg>
 __device__ __forceinline__ void fit_issue_row(const FitArgs& a, int f, int by, int sg, int rr, float* dst,
                                               uint64_t* bar, uint64_t pol_g, uint64_t pol_y)
 {
-    constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats of stage per guide plane
-    mbar_arrive_expect_tx(bar, (Q * GF + (3 + (MOD ? 3 : 0)) * kSeg) * 4);
-    const int x = sg * kSeg, y = by * D + rr;
+    constexpr int GF = HG ? SW / 2 : SW;  // floats of stage per guide plane
+    mbar_arrive_expect_tx(bar, (Q * GF + (3 + (MOD ? 3 : 0)) * SW) * 4);
+    const int x = sg * SW, y = by * D + rr;
     tma_load_3d(dst, &a.tg, x, y, f * Q, bar, pol_g);
     tma_load_3d(dst + Q * GF, &a.ty, x, y, f * 3, bar, pol_y);
-    if (MOD) tma_load_3d(dst + Q * GF + 3 * kSeg, &a.ta, x, y, f * 3, bar, pol_y);
+    if (MOD) tma_load_3d(dst + Q * GF + 3 * SW, &a.ta, x, y, f * 3, bar, pol_y);
 }
 
 // packed-pair layout of the FIT accumulators: d is paired over planes (2p, 2p+1)
