@@ -66,6 +66,13 @@ __device__ __forceinline__ void ws_proxy_fence()
 #endif
 }
 
+__device__ __forceinline__ int smid()
+{
+    int v;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+    return v;
+}
+
 __device__ __forceinline__ long long gtimer()
 {
     long long t;
@@ -78,8 +85,10 @@ __device__ __forceinline__ long long gtimer()
 // grid-dependency wait, 2 = exit.  Compiled out of the library.
 #ifdef FLR_TIMELINE
 __device__ long long g_flr_tl[3 * 1024 * 4];  // single-TU tools only (no -rdc)
-#define FLR_TL(k, slot) \
-    (g_flr_tl[((k) * 1024 + blockIdx.x + blockIdx.y * gridDim.x) * 4 + (slot)] = gtimer())
+#define FLR_TL(k, slot)                                                                           \
+    (((slot) == 2 ? (void)(g_flr_tl[((k) * 1024 + blockIdx.x + blockIdx.y * gridDim.x) * 4 + 3] = smid()) \
+                  : (void)0),                                                                          \
+     g_flr_tl[((k) * 1024 + blockIdx.x + blockIdx.y * gridDim.x) * 4 + (slot)] = gtimer())
 #else
 #define FLR_TL(k, slot) ((void)0)
 #endif

@@ -83,5 +83,13 @@ int main(int argc, char** argv)
                nm[k], ncta[k], (emin - t0) * 1e-3, (emax - t0) * 1e-3, (wmin - t0) * 1e-3, (wmax - t0) * 1e-3,
                (xmin - t0) * 1e-3, (xmax - t0) * 1e-3, dur / ncta[k] * 1e-3);
     }
+    if (argc > 1 && std::string(argv[1]) == "cta") {  // fit: per-CTA exit (relative), SM id, items
+        std::vector<std::pair<long long, int>> ex;
+        for (int c = 0; c < ncta[0]; ++c) ex.push_back({tl[c * 4 + 2] - t0, c});
+        std::sort(ex.begin(), ex.end());
+        printf("fit CTA exits (us: cta/sm):");
+        for (auto& e : ex) printf(" %.1f:%d/%lld", e.first * 1e-3, e.second, tl[e.second * 4 + 3]);
+        printf("\n");
+    }
     return 0;
 }
