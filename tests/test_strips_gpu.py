@@ -51,3 +51,17 @@ def test_strips_1080p_eight_parts_match_full_frame():
     assert torch.isfinite(got).all()
     assert_parity(got.cpu().numpy(), full.cpu().numpy().astype(np.float64), "1080p strips vs full")
     print(f"1080p strips bitwise equal to full frame: {torch.equal(got, full)}")
+
+
+def test_strips_fp16_guides_match_full_frame():
+    """fp16 guide planes through the strip path: same kernels per strip."""
+    import paper_2410_11625_b200 as flr
+    from paper_2410_11625_b200 import strips, synth
+
+    G, Y = synth.frame(960, 544, Q=8, seed=31, device="cuda")
+    g, y = G.half().unsqueeze(0).contiguous(), Y.unsqueeze(0).contiguous()
+    R = flr.effective_radius(block=D, sigma=SIGMA)
+    got = strips.denoise_strips_local(_gpu_fn(flr), g, y, D, R, 4)
+    full = _gpu_fn(flr)(g, y)
+    torch.cuda.synchronize()
+    assert_parity(got.cpu().numpy(), full.cpu().numpy().astype(np.float64), "fp16 strips vs full")
