@@ -50,7 +50,9 @@ def test_strips_1080p_eight_parts_match_full_frame():
     torch.cuda.synchronize()
     assert torch.isfinite(got).all()
     assert_parity(got.cpu().numpy(), full.cpu().numpy().astype(np.float64), "1080p strips vs full")
-    print(f"1080p strips bitwise equal to full frame: {torch.equal(got, full)}")
+    # the strips run the full frame's kernels on a sub-grid of its blocks: same arithmetic,
+    # same order (measured bitwise equal on B200)
+    assert torch.equal(got, full)
 
 
 def test_strips_fp16_guides_match_full_frame():
