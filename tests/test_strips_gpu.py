@@ -67,3 +67,29 @@ def test_strips_fp16_guides_match_full_frame():
     full = _gpu_fn(flr)(g, y)
     torch.cuda.synchronize()
     assert_parity(got.cpu().numpy(), full.cpu().numpy().astype(np.float64), "fp16 strips vs full")
+
+
+@pytest.mark.parametrize("W,H,Q,sigma,block", [(7680, 4320, 8, 20.0, 8), (8192, 8192, 4, 10.0, 8)])
+def test_max_size_frame_sampled_by_oracle_strips(oracle_mod, W, H, Q, sigma, block):
+    """Maximum sizes (8K UHD with the C3 window; a 64-Mpixel square): the GPU denoises the
+    whole frame; the oracle, too slow for the frame, denoises three block-row bands (top,
+    middle, bottom) each extended by the (R + 1)-block halo -- which reproduces its own
+    full-frame rows bitwise (test_strips.py) -- and the GPU's rows must match them."""
+    import paper_2410_11625_b200 as flr
+    from paper_2410_11625_b200 import strips, synth
+
+    G, Y = synth.frame(W, H, Q=Q, seed=8000 + Q, device="cuda")
+    g, y = G.unsqueeze(0).contiguous(), Y.unsqueeze(0).contiguous()
+    del G, Y
+    out = flr.denoise(g, y, block=block, sigma=sigma)
+    torch.cuda.synchronize()
+    R = flr.effective_radius(block=block, sigma=sigma)
+    h = strips.halo_blocks(R) * block
+    By = -(-H // block)
+    for b_lo in (0, By // 2, By - 4):
+        lo, hi = b_lo * block, min(H, (b_lo + 4) * block)
+        ilo, ihi = max(0, lo - h), min(H, hi + h)
+        ref = oracle_mod.denoise(g[..., ilo:ihi, :].cpu().numpy(), y[..., ilo:ihi, :].cpu().numpy(),
+                                 D=block, sigma=sigma, R=R)
+        assert_parity(out[..., lo:hi, :].cpu().numpy(), ref[..., lo - ilo:hi - ilo, :],
+                      f"{W}x{H} rows {lo}-{hi}")
