@@ -108,6 +108,8 @@ def gather_frame(own_out, plan, group=None):
     """All-gather every rank's own rows into the full frame [..., H, W] (rows padded to
     the tallest strip for the collective, then trimmed)."""
     world = len(plan)
+    if world == 1:
+        return own_out
     rows = max(p[1] - p[0] for p in plan)
     lead, W = own_out.shape[:-2], own_out.shape[-1]
     pad = torch.zeros(*lead, rows, W, dtype=own_out.dtype, device=own_out.device)

@@ -71,6 +71,16 @@ def test_short_halo_differs(oracle_mod, monkeypatch):
     assert not torch.equal(got, full)
 
 
+def test_single_rank_needs_no_process_group(oracle_mod):
+    """world = 1: no halo, no exchange, no collective -- the whole-frame call."""
+    G, Y = _frame(40, 48)
+    plan = strips.strip_plan(48, D, R, 1)
+    assert plan == [(0, 48, 0, 48)]
+    fn = _oracle_fn(oracle_mod)
+    got = strips.denoise_strip(fn, G, Y, plan, 0, gather=True)
+    assert torch.equal(got, fn(G, Y))
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
