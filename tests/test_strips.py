@@ -108,8 +108,10 @@ def _worker(rank, world, port, W, H, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_gloo_strips_match_full_frame(oracle_mod):
-    world, W, H = 2, 40, 72
+@pytest.mark.parametrize("world,W,H", [(2, 40, 72), (3, 24, 101)])
+def test_gloo_strips_match_full_frame(oracle_mod, world, W, H):
+    """world 2, and world 3 (the middle rank exchanges with both neighbours; a partial
+    last block row)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
