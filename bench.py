@@ -13,9 +13,13 @@ CUDA events on the launching stream; the max over ranks is reported.  Per-kernel
 durations (for the roofline of the dominant kernel) come from caller-owned CUDA
 events the library records between its launches inside the same timed region.
 
-Multi-GPU (torchrun, one rank per GPU): frames are independent, so every rank
-denoises its own frames (weak scaling); NCCL only carries the timing max and
-checksums after the timed region.
+Multi-GPU (one rank per GPU; `--gpus N` outside torchrun re-launches itself under
+torch.distributed.run): frames are independent, so every rank denoises its own frames
+and NCCL only carries the timing max and checksums after the timed region.  c2 (the
+default) gives every rank one frame per step (weak scaling); c5 is the fixed 256-frame
+batch split by dist.shard_range (strong scaling) with per-frame checksums gathered in
+global frame order (identical for every G: each frame's arithmetic does not depend on
+the batch it runs in).
 
 --impl reference times the fp64 CPU oracle (oracle/flr_ref.c) on the host cores on
 a bounded sample of the same workload (a band of rows of the frame per step).
@@ -47,8 +51,8 @@ CONFIGS = {
                block=8, upsample=1, sigma=20.0),
     "c4": dict(workload="C4 joint denoise+2x upsample: 960x540 1spp radiance, 1920x1080 guides, Q=8",
                W=960, H=540, Q=8, block=4, upsample=2, sigma=10.0),
-    "c5": dict(workload="C5 batch of 1080p frames (Q=8, 8x8) frame-sharded over GPUs", W=1920, H=1080, Q=8,
-               block=8, upsample=1, sigma=10.0),
+    "c5": dict(workload="C5 batch of 256 1080p frames (Q=8, 8x8) frame-sharded over GPUs", W=1920, H=1080, Q=8,
+               block=8, upsample=1, sigma=10.0, batch=256),
 }
 
 
@@ -60,7 +64,7 @@ def parse():
     ap.add_argument("--impl", choices=["flr", "reference"], default="flr")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--frames-per-step", type=int, default=None,
-                    help="frames per step per GPU (default 1; c5: 32)")
+                    help="frames per call per GPU (default 1; c5: 32-frame calls over the rank's shard)")
     ap.add_argument("--pool", type=int, default=0, help="distinct frames rotated (0 = auto, > 2x L2)")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=20)
@@ -76,6 +80,9 @@ def parse():
     ap.add_argument("--guides", choices=["f32", "f16"], default="f32",
                     help="guide plane precision (f16: the fp16 guide network's output, SURVEY f2)")
     return ap.parse_args()
+
+
+METRIC = "Mpixel/s (FLR fit+apply, 1spp) and ms per frame; % of HBM BW"
 
 
 # --------------------------------------------------------------------------- helpers
@@ -240,7 +247,7 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_sample(cfg, budget_s, seed=777):
+def oracle_sample(cfg, budget_s, seed=777, one_thread=False):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload: bands of
     full-width rows of the frame (multiples of the block size), until ~budget_s."""
     import numpy as np
@@ -268,7 +275,20 @@ def oracle_sample(cfg, budget_s, seed=777):
         run()
         times.append(time.perf_counter() - t0)
     tot = sum(times)
+    one = None
+    if one_thread:  # the same sample on one host thread
+        n_thr = oracle.num_threads()
+        oracle.set_num_threads(1)
+        try:
+            t0 = time.perf_counter()
+            run()
+            t1 = time.perf_counter() - t0
+        finally:
+            oracle.set_num_threads(n_thr)
+        one = {"value": px / t1 / 1e6, "unit": "Mpixel/s", "cores": 1, "sample": f"1 band of {W}x{band} px",
+               "ms_per_frame_extrapolated": 1e3 * t1 * (cfg["H"] / band)}
     return {"value": px * len(times) / tot / 1e6, "unit": "Mpixel/s", "cores": oracle.num_threads(),
+            "one_thread": one,
             "kind": "oracle", "cpu": cpu_model(),
             "sample": f"{len(times)} bands of {W}x{band} px{' (x%d upsample)' % U if U > 1 else ''} "
                       f"of the {cfg['workload'].split(' ')[0]} workload, {tot:.1f} s",
@@ -276,6 +296,12 @@ def oracle_sample(cfg, budget_s, seed=777):
 
 
 # --------------------------------------------------------------------------- reference arm
+def ref_config(cfg, R):
+    """The config keys both arms print (so the driver can pair the lines)."""
+    return {"workload": cfg["workload"], "W": cfg["W"], "H": cfg["H"], "Q": cfg["Q"], "block": cfg["block"],
+            "upsample": cfg["upsample"], "sigma": cfg["sigma"], "radius": R, "eps_add": 1e-5, "eps_mul": 1e-4}
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
@@ -308,12 +334,12 @@ def run_reference(args, cfg, rank, world):
     px = W * rows * U * U
     value = px * args.steps / dt / 1e6
     line = {
-        "impl": "reference", "metric": "Mpixel/s (FLR fit+apply, 1spp, fp64 CPU oracle)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "strong" if cfg.get("batch") else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
-        "config": {"workload": cfg["workload"], "sample": f"{W}x{rows} band per step", "Q": Q, "block": D,
-                   "upsample": U, "sigma": sigma, "radius": R},
+        "config": ref_config(cfg, R), "sample": f"{W}x{rows} band of the frame per step (fp64 CPU oracle)",
         "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": oracle.num_threads(), "kind": "oracle",
                          "sample": f"{args.steps} steps of a {W}x{rows} band", "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -322,6 +348,37 @@ def run_reference(args, cfg, rank, world):
 
 
 # --------------------------------------------------------------------------- FLR arm
+def batch_plan(batch, rank, world, frames_per_call=32):
+    """c5's rank loop plan: rank `rank` of `world` owns frames [lo, hi) of the
+    global batch (dist.shard_range), seeded by global frame index; it denoises them in
+    `pool` calls of F frames (F = the largest divisor of its shard <= frames_per_call)."""
+    from paper_2410_11625_b200 import dist as fd
+
+    lo, hi = fd.shard_range(batch, rank, world)
+    nsh = hi - lo
+    cap = max(1, min(frames_per_call, nsh))
+    F = max(d for d in range(1, cap + 1) if nsh % d == 0)
+    return lo, hi, F, nsh // F, [1000 + g for g in range(lo, hi)]
+
+
+def batch_checksums(call, pool, lo, batch, device=None):
+    """Per-frame checksums of the rank's `pool` calls (call(i) returns the [F, 3, H, W]
+    output of its i-th call), gathered in global frame order and digested: identical for
+    every world size, since each frame's arithmetic does not depend on its batch."""
+    import hashlib
+
+    import torch
+
+    from paper_2410_11625_b200 import dist as fd
+
+    rows = torch.cat([fd.per_frame_checksums(call(i)) for i in range(pool)]) if pool else torch.zeros(0, 3)
+    full = fd.gather_frame_checksums(rows, lo, batch, device=device)
+    return {"frames": batch, "sha256": hashlib.sha256(full.numpy().tobytes()).hexdigest(),
+            "all_finite": bool(torch.isfinite(full).all() and (full[:, 2] == 1).all()),
+            "frame0": full[0].tolist(), "frame_last": full[-1].tolist(),
+            "note": "[sum, max|x|, finite] per frame in global order; identical for every G"}
+
+
 def run_flr(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -332,17 +389,25 @@ def run_flr(args, cfg, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     W, H, Q, D, U, sigma = cfg["W"], cfg["H"], cfg["Q"], cfg["block"], cfg["upsample"], cfg["sigma"]
-    F = args.frames_per_step or (32 if args.config == "c5" else 1)
     half = args.guides == "f16"
     gbytes = cfg["gbytes"]
     frame_in_bytes = (Q * gbytes + 3 * 4) * W * H + (Q * gbytes * W * H * U * U if U > 1 else 0)
-    pool = args.pool or max(2, math.ceil(2.5 * L2_BYTES / (frame_in_bytes * F)))
     R = flr.effective_radius(block=D, upsample=U, sigma=sigma)
-
-    # ---- inputs resident in HBM (global frame index -> seed; ranks draw disjoint frames)
     from paper_2410_11625_b200 import dist as fd
 
-    seeds = fd.frame_seeds(rank, world, pool * F)
+    batch = cfg.get("batch")
+    if batch:  # c5: the fixed global batch, split by frame (strong scaling); a step = one pass over it
+        lo, hi, F, pool, seeds = batch_plan(batch, rank, world, args.frames_per_step or 32)
+        nsh = hi - lo
+        K = args.steps * pool
+    else:  # one call per step on `frames_per_step` frames of a rotating pool (> 2x L2)
+        lo, hi, nsh = 0, 0, 0
+        F = args.frames_per_step or 1
+        pool = args.pool or max(2, math.ceil(2.5 * L2_BYTES / (frame_in_bytes * F)))
+        seeds = fd.frame_seeds(rank, world, pool * F)  # ranks draw disjoint global frames
+        K = args.steps
+
+    # ---- inputs resident in HBM (global frame index -> seed)
     gl, yl, gh, al, dl = [], [], [], [], []
     for i in range(pool):
         if args.modulated:  # the renderer's outputs: modulated radiance, albedo, direct light
@@ -415,7 +480,6 @@ def run_flr(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
 
     # ---- CUDA graphs: a full pool rotation and the remainder (timed), a traced rotation
-    K = args.steps
     use_graph = not args.no_graph
     graphs = {}
     if use_graph:
@@ -555,7 +619,8 @@ def run_flr(args, cfg, rank, world, local_rank):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms / E, "steps": E,
                "pipeline": "h2d / denoise / d2h on 3 streams, double-buffered (pinned host memory)"}
 
-    # ---- checksums of one output per rank, gathered over NCCL (the only collective)
+    # ---- per-frame checksums gathered over NCCL in global frame order (the only collective)
+    frame_cs = batch_checksums(call, pool, lo, batch, device=dev) if batch else None
     o = call(0)
     torch.cuda.synchronize()
     allcs = fd.gather_rows(fd.output_checksum(o), device=dev)
@@ -563,7 +628,7 @@ def run_flr(args, cfg, rank, world, local_rank):
     if rank != 0:
         return
     peak, peak_src = load_peaks()
-    frames_total = world * K * F
+    frames_total = args.steps * batch if batch else world * K * F
     px_total = frames_total * out_pixels(cfg)
     value = px_total / (ms_max * 1e-3) / 1e6
     # dominant kernel (largest share of the step) and its own algorithmic bytes
@@ -598,22 +663,23 @@ def run_flr(args, cfg, rank, world, local_rank):
             a_ = KERNEL_FLOPS[n](cfg) * F / (t * 1e-3) / 1e12
             kroof[n] = {"bound": "alu", "achieved": a_, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s (fp64)",
                         "frac": a_ / FP64_PEAK_TFLOPS, "avg_launch_us": t * 1e3}
-    step_ms = ms_max / K
-    step_bytes = min_bytes_per_frame(cfg) * F
+    step_ms = ms_max / args.steps  # c5: one pass over the rank's shard of the batch
+    step_bytes = min_bytes_per_frame(cfg) * (nsh if batch else F)
     step_roof = {"min_bytes_per_step": step_bytes, "achieved": step_bytes / (step_ms * 1e-3) / 1e9,
                  "peak": peak, "unit": "GB/s", "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak}
     cpu_base = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu_base = oracle_sample(cfg, args.cpu_seconds)
+        cpu_base = oracle_sample(cfg, args.cpu_seconds, one_thread=True)
+    frames_per_step = batch if batch else world * F
     line = {
-        "metric": "Mpixel/s (FLR fit+apply, 1spp) and ms per frame; % of HBM BW",
-        "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": step_ms, "ms_per_frame": step_ms / F, "frames_per_s": frames_total / (ms_max * 1e-3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC,
+        "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "ms_per_frame": ms_max / frames_total, "frames_per_s": frames_total / (ms_max * 1e-3),
+        "higher_is_better": True, "scaling": "strong" if batch else "weak", "vs_baseline": None,
         "dtype": "f32" if not half else "f32 (fp16 guide planes)", "data": "synthetic (seeded procedural Lambertian scenes, rasterised guides, 1spp noise)",
-        "config": {"workload": cfg["workload"], "W": W, "H": H, "Q": Q, "block": D, "upsample": U, "sigma": sigma,
-                   "radius": R, "eps_add": 1e-5, "eps_mul": 1e-4, "frames_per_step": F, "global_batch": world * F,
-                   "pool_frames": pool, "l2": f"rotating pool of {pool} distinct steps "
+        "config": {**ref_config(cfg, R), "frames_per_call": F, "calls_per_step": pool if batch else 1,
+                   "global_batch": frames_per_step, "shard": [lo, hi] if batch else None,
+                   "pool_frames": pool * F, "l2": f"inputs rotate through {pool * F} distinct resident frames "
                    f"({pool * F * frame_in_bytes / 1e6:.0f} MB > 126 MB L2)", "graphs": use_graph,
                    "parallelism": f"frame-sharded dp{world}", "variant": args.variant,
                    "guides": args.guides, "modulated": bool(args.modulated),
@@ -625,7 +691,7 @@ def run_flr(args, cfg, rank, world, local_rank):
         "kernel_roofline": kroof,
         "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": launches_per_step * K,
         "clocks": clocks,
-        "checksums": allcs,
+        "checksums": allcs, "frame_checksums": frame_cs,
         "paper_context": {"rtx2080ti_ms_per_1080p_frame": 0.636, "source": "P:429 (Table 1)"},
     }
     if check is not None:
@@ -645,9 +711,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            sys.exit(f"--gpus {args.gpus} needs torchrun --nproc-per-node {args.gpus}")
+        sys.exit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

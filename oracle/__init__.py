@@ -104,6 +104,13 @@ def num_threads() -> int:
     return lib().flr_ref_num_threads()
 
 
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count of later oracle calls from this thread (libgomp's
+    omp_set_num_threads; the oracle's results do not depend on it)."""
+    lib()
+    ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+
+
 def moments(guides, radiance, D):
     """Block sums (M [n,By,Bx,P,P], N [n,By,Bx,P,3])."""
     g, r = _frames(guides, radiance)

@@ -198,7 +198,7 @@ def _ptr(t):
 
 
 def fit(guides, radiance, *, block=8, upsample=1, sigma=10.0, radius=0, eps_add=1e-5,
-        eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None, workspace=None):
+        eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, flags=0, out=None, workspace=None):
     """Per-block raw-basis models [n, By, Bx, Q+1, 3].
     float16 guides (the fp16 guide network's output) take the fp16 streaming path."""
     torch = _torch()
@@ -207,7 +207,7 @@ def fit(guides, radiance, *, block=8, upsample=1, sigma=10.0, radius=0, eps_add=
     n, Q, H, W = g.shape
     if tuple(y.shape) != (n, 3, H, W):
         raise ValueError("radiance must be [n,3,H,W] matching guides")
-    p = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver)
+    p = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver, flags)
     Bx, By = math.ceil(W / block), math.ceil(H / block)
     if out is None:
         out = torch.empty((n, By, Bx, Q + 1, 3), dtype=torch.float32, device=g.device)
@@ -241,7 +241,7 @@ def apply(models, guides, block_out, *, out=None):
 
 
 def denoise(guides, radiance, *, block=8, sigma=10.0, radius=0, eps_add=1e-5, eps_mul=1e-4,
-            variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None, workspace=None):
+            variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, flags=0, out=None, workspace=None):
     """FLR denoise: fit + apply with the same guides.  [n,Q,H,W], [n,3,H,W] -> [n,3,H,W].
     Guides may be float16 (fp16 streaming path)."""
     torch = _torch()
@@ -250,7 +250,7 @@ def denoise(guides, radiance, *, block=8, sigma=10.0, radius=0, eps_add=1e-5, ep
     n, Q, H, W = g.shape
     if tuple(y.shape) != (n, 3, H, W):
         raise ValueError("radiance must be [n,3,H,W] matching guides")
-    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, variant, solver)
+    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, variant, solver, flags)
     if out is None:
         out = torch.empty((n, 3, H, W), dtype=torch.float32, device=g.device)
     ws_bytes = workspace_size(n, Q, W, H, block=block, sigma=sigma, radius=radius, eps_add=eps_add,
@@ -263,7 +263,7 @@ def denoise(guides, radiance, *, block=8, sigma=10.0, radius=0, eps_add=1e-5, ep
 
 
 def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, sigma=10.0, radius=0,
-                     eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, out=None,
+                     eps_add=1e-5, eps_mul=1e-4, variant=VARIANT_AUTO, solver=SOLVER_APPENDIX, flags=0, out=None,
                      workspace=None):
     """Joint denoise + upsample: fit on low-res radiance/guides, apply with hi-res guides.
     With upsample=1 this is FLNR's split-guide call (fit on X'_model, apply X'_map).
@@ -278,7 +278,7 @@ def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, 
     Hh, Wh = int(gh.shape[2]), int(gh.shape[3])
     if tuple(y.shape) != (n, 3, H, W) or gh.shape[0] != n or gh.shape[1] != Q:
         raise ValueError("shape mismatch between guides_lo, radiance_lo and guides_hi")
-    p = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver)
+    p = Params.make(block, upsample, sigma, radius, eps_add, eps_mul, variant, solver, flags)
     if out is None:
         out = torch.empty((n, 3, Hh, Wh), dtype=torch.float32, device=g.device)
     ws_bytes = workspace_size(n, Q, W, H, block=block, upsample=upsample, sigma=sigma, radius=radius,
@@ -291,7 +291,7 @@ def denoise_upsample(guides_lo, radiance_lo, guides_hi, *, block=4, upsample=2, 
 
 
 def denoise_modulated(guides, radiance_mod, albedo, direct=None, *, block=8, sigma=10.0, radius=0,
-                      eps_add=1e-5, eps_mul=1e-4, albedo_floor=1e-3, solver=SOLVER_APPENDIX, out=None,
+                      eps_add=1e-5, eps_mul=1e-4, albedo_floor=1e-3, solver=SOLVER_APPENDIX, flags=0, out=None,
                       workspace=None):
     """The paper's protocol: demodulate by max(albedo, floor), FLR-denoise,
     remodulate, add the direct light.  All radiance-like tensors are [n,3,H,W]."""
@@ -304,7 +304,7 @@ def denoise_modulated(guides, radiance_mod, albedo, direct=None, *, block=8, sig
     for t, nm in ((r, "radiance_mod"), (a, "albedo")) + (((d, "direct"),) if d is not None else ()):
         if tuple(t.shape) != (n, 3, H, W):
             raise ValueError(f"{nm} must be [n,3,H,W] matching guides")
-    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, VARIANT_AUTO, solver)
+    p = Params.make(block, 1, sigma, radius, eps_add, eps_mul, VARIANT_AUTO, solver, flags)
     if out is None:
         out = torch.empty((n, 3, H, W), dtype=torch.float32, device=g.device)
     ws_bytes = workspace_size(n, Q, W, H, block=block, sigma=sigma, radius=radius, eps_add=eps_add,

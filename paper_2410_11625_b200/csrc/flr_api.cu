@@ -49,7 +49,7 @@ int effective_radius(const flr_params* p)
 }
 
 struct Layout {
-    size_t raw, mom, hb, models, flags, total;
+    size_t raw, mom, hb, models, total;
 };
 
 // workspace: raw fp32 moments | fp64 un-shifted moments | fp64 x-blurred | padded models
@@ -67,8 +67,6 @@ Layout layout(int n, int Q, int Bx, int By)
     off += align256(nbp * km_of(Q) * sizeof(double));
     L.models = off;
     off += align256(nb * mstride_of(Q) * sizeof(float));
-    L.flags = off;  // row counters: fit_done [n][By] + K2/solve_done [n][ceil(By/4)] (wavefronts)
-    off += align256(sizeof(int) * (size_t)n * (By + (By + 3) / 4));
     L.total = off;
     return L;
 }
@@ -147,7 +145,8 @@ flr_status check_ws(int n, int Q, int W, int H, const flr_params* p, void* ws, s
 
 // fit into `models` with `mstride` floats per block; arguments already validated
 flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, const flr_params* p,
-                  float* models, int mstride, void* ws, LaunchCtx& ctx, bool hg = false)
+                  float* models, int mstride, void* ws, LaunchCtx& ctx, bool hg = false,
+                  bool inputs_from_call = false)
 {
     const int D = p->block;
     const int Bx = cdiv(W, D), By = cdiv(H, D);
@@ -155,11 +154,9 @@ flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, co
     char* base = (char*)ws;
     const double sblk = p->sigma / ((double)D * p->upsample);
     const Taps taps = make_taps(sblk, effective_radius(p));
-    // opt-in row wavefront across the three grids (FLR_WAVE=1): measured slower on one
-    // B200 (the per-item release and the per-call flag reset cost more than the overlap)
-    static const bool wave = std::getenv("FLR_WAVE") != nullptr;
-    ctx.wave_flags = wave ? (int*)(base + L.flags) : nullptr;
-    ctx.early = (p->flags & FLR_FLAG_INPUTS_READY) && !wave;
+    // FLR_FLAG_INPUTS_READY: the moment grid may stream before its grid-dependency wait --
+    // unless its radiance was produced inside this call (the unfused demodulation)
+    ctx.early = (p->flags & FLR_FLAG_INPUTS_READY) && !inputs_from_call;
     FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, G, Y, (float*)(base + L.raw),
                                       (double*)(base + L.mom), (double*)(base + L.hb), models,
                                       mstride, p->eps_add, solver_eps_mul(p), taps, ctx, nullptr, 0.f, hg)));
@@ -310,22 +307,7 @@ flr_status denoise_upsample_impl(int32_t n, int32_t Q, int32_t W_lo, int32_t H_l
     float* models = (float*)((char*)workspace + L.models);
     const int ms = mstride_of(Q);
     LaunchCtx ctx = make_ctx(stream, trace);
-    // AUTO currently resolves to STAGED: on B200 the fused wavefront kernel is still
-    // solver-bound; it is selected explicitly with FUSED.
-    if (p->variant == FLR_VARIANT_FUSED) {
-        FusedLaunch F;
-        F.n = n, F.W = W_lo, F.H = H_lo, F.D = D, F.U = p->upsample, F.Bx = Bx, F.By = By;
-        F.G = guides_lo, F.Y = radiance_lo, F.Gout = guides_hi, F.out = out;
-        F.mom = (double*)((char*)workspace + L.mom);
-        F.models = models;
-        F.flags = (int*)((char*)workspace + L.flags);
-        F.eps_add = p->eps_add, F.eps_mul = solver_eps_mul(p);
-        F.taps = make_taps(p->sigma / ((double)D * p->upsample), effective_radius(p));
-        bool done = false;
-        FLR_DISPATCH_Q(Q, (done = launch_fused<QQ>(F, ctx)));
-        if (done) return finish(ctx, trace);
-        if (p->variant == FLR_VARIANT_FUSED) return FLR_ERR_UNSUPPORTED;
-    }
+    if (p->variant == FLR_VARIANT_FUSED) return FLR_ERR_UNSUPPORTED;
     const int Dout = D * p->upsample;
     if (hg && (!half_guides_fit_ok(D, W_lo, guides_lo, radiance_lo) ||
                !half_guides_apply_ok(Dout, W_hi, models, guides_hi, out)))
@@ -453,7 +435,7 @@ flr_status flr_denoise_modulated_traced(int32_t n, int32_t Q, int32_t W, int32_t
     } else {  // demodulate into `out` (same shape), then the plain fit reads it
         ctx.before("k_demod");
         k_demod<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(total, radiance_mod, albedo, albedo_floor, out);
-        if ((st = do_fit(n, Q, W, H, guides, out, p, models, ms, workspace, ctx))) return st;
+        if ((st = do_fit(n, Q, W, H, guides, out, p, models, ms, workspace, ctx, false, true))) return st;
     }
     bool mod_ok = false;
     FLR_DISPATCH_Q(Q, (mod_ok = apply_mod_supported<QQ>()));

@@ -179,10 +179,11 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     __syncthreads();
     const int per_frame = a.By * a.nseg, nitems = n * per_frame, GW = gridDim.x * NC;
     // Default: the inputs may come from the previous grid, so wait for it before streaming.
-    // Early (inputs ready before the previous grid began): stream at once, and run the wait
-    // (+ trigger) once this CTA has issued its last row, so the dependents -- K2, which writes
-    // the models the previous call's apply may still be reading -- launch only after the
-    // previous grid completed.
+    // Early (inputs ready before the previous grid began): the producer streams at once and
+    // runs the wait (+ trigger) once it has issued its last row, so the dependents -- K2,
+    // which writes the models the previous call's apply may still be reading -- launch only
+    // after the previous grid completed.  The consumers also wait before their first store
+    // to the moment field, which the previous grid (a K2 reading it by TMA) may still read.
     if (!a.early) {
         pdl_wait();  // caller data may come from the previous grid
         pdl_trigger();  // dependents launch only once we are past our own wait
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
         // ---------------- producer: lane c feeds consumer c ----------------
         if (lane >= NC) return;
         const int c = lane;
-        const uint64_t pg = policy_by_code(a.gpol), py = policy_evict_first();
+        const uint64_t pg = policy_evict_first(), py = policy_evict_first();
         int it = blockIdx.x * NC + c, row = 0, rows = 0, f = 0, by = 0, sg = 0;
         auto decode = [&]() {
             if (it >= nitems) return;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     const int w = warp;
     float* ring = stages + (size_t)w * S * STG;
     int k = 0;  // rows consumed
+    bool waited = !a.early;  // past the grid-dependency wait (early mode: before the first store)
     for (int it = blockIdx.x * NC + w; it < nitems; it += GW) {
         const int f = it / per_frame, rem = it - f * per_frame, by = rem / a.nseg, sg = rem - by * a.nseg;
         const int rows = min(D, a.H - by * D);
@@ -252,6 +254,10 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
         fold_pairs(acc.S, sv, DQ);
         fold_pairs(acc.Y, yc, DQ);
         fold_pairs(acc.XY, xy, DQ);
+        if (!waited) {
+            pdl_wait();
+            waited = true;
+        }
         if (bx < a.Bx) {
         const int gi = lane % DQ;
         const double nn = (double)(min(D, a.W - bx * D) * rows);
@@ -281,10 +287,6 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
 #pragma unroll
             for (int c = 0; c < 3; ++c)
                 put(Dm::C_XY + j * 3 + c, fma((double)cs[j], (double)yc[c], (double)xy[j * 3 + c]));
-        }
-        if (a.done) {
-            __syncwarp();
-            if (lane == 0) red_release_add(&a.done[f * a.By + by], 1);
         }
     }
     if (threadIdx.x == 0) FLR_TL(0, 2);

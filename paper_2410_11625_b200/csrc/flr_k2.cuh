@@ -60,8 +60,7 @@ struct K2Geom {
 template <int Q, int R>
 __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
     k_blur_solve_tile(const __grid_constant__ CUtensorMap tm, int Bx, int By, float* __restrict__ models,
-                      double eps_add, double eps_mul, const __grid_constant__ Taps t, const int* wait_rows,
-                      int wait_target, int* signal, int kpol)
+                      int mstride, double eps_add, double eps_mul, const __grid_constant__ Taps t)
 {
     using Dm = Dims<Q>;
     using KG = K2Geom<Q, R>;
@@ -84,24 +83,15 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
         uint64_t* b = &bar[grp % S];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage before
         mbar_arrive_expect_tx(b, KG::BOXD * sizeof(double));
-        tma_load_3d(ring + (grp % S) * KG::BOX, &tm, bx0 - RE, by0 - R, f * KM + grp * G, b, policy_by_code(kpol));
+        tma_load_3d(ring + (grp % S) * KG::BOX, &tm, bx0 - RE, by0 - R, f * KM + grp * G, b, policy_evict_normal());
     };
     if (tid == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
     }
-    if (!wait_rows) {
-        pdl_wait();  // the moment field comes from the previous grid
-        pdl_trigger();  // dependents launch only once we are past our own wait
-        if (tid == 0) FLR_TL(1, 1);
-    } else {
-        pdl_trigger();  // wavefront: wait only for the FIT rows this tile reads (+- R), one thread per row
-        const int rr = by0 - R + tid;
-        if (tid < TY + 2 * R && rr >= 0 && rr < By)
-            while (ld_acquire(&wait_rows[f * By + rr]) < wait_target) __nanosleep(64);
-        __syncthreads();
-        if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
-    }
+    pdl_wait();  // the moment field comes from the previous grid
+    pdl_trigger();  // dependents launch only once we are past our own wait
+    if (tid == 0) FLR_TL(1, 1);
     __syncthreads();
     if (tid == 0)
         for (int g = 0; g < S && g < NG; ++g) issue(g);
@@ -195,33 +185,23 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
         g_flr_phase[63] = NG + 3;
     }
 #endif
-    const int nbx = min(TX, Bx - bx0);
+    const int nbx = min(TX, Bx - bx0), nrow = min(TY, By - by0);
     static_assert(MS % 4 == 0, "padded models are whole float4s");
-#ifndef FLR_K2_SCALAR_STORE
-    {  // the tile's rows are contiguous runs of nbx models (16-byte aligned): float4 stores
-        const int nrow = min(TY, By - by0), q = nbx * (MS / 4);
+    if (mstride == MS && (reinterpret_cast<uintptr_t>(models) & 15) == 0) {  // rows: contiguous aligned runs
+        const int q = nbx * (MS / 4);
         for (int i = tid; i < nrow * q; i += kK2Threads) {
             const int r = i / q, j = i - r * q;
             reinterpret_cast<float4*>(models + ((size_t)(f * By + by0 + r) * Bx + bx0) * MS)[j] =
                 reinterpret_cast<const float4*>(mstage + r * TX * MS)[j];
         }
+    } else {  // the ABI's packed [Q+1][3] models (flr_fit): runs of nbx * mstride floats, 4-byte aligned
+        const int q = nbx * mstride;
+        for (int i = tid; i < nrow * q; i += kK2Threads) {
+            const int r = i / q, j = i - r * q, b = j / mstride;
+            models[((size_t)(f * By + by0 + r) * Bx + bx0) * mstride + j] = mstage[(r * TX + b) * MS + j - b * mstride];
+        }
     }
-#else
-    for (int r = 0; r < TY && by0 + r < By; ++r) {  // one contiguous run of nbx models per row
-        float* dst = models + ((size_t)(f * By + by0 + r) * Bx + bx0) * MS;
-        const float* src = mstage + r * TX * MS;
-        for (int i = tid; i < nbx * MS; i += kK2Threads) dst[i] = src[i];
-    }
-#endif
-#ifdef FLR_DBG_PHASES
-    __syncthreads();
-    if (tid == 0) g_flr_phase[1000 + 4 * cta_id + 1] = gtimer(), g_flr_phase[1000 + 4 * cta_id + 2] = tsg[NG + 2] - tsg[0];
-#endif
     if (tid == 0) FLR_TL(1, 2);
-    if (signal) {  // publish this tile's models to the APPLY wavefront
-        __syncthreads();
-        if (tid == 0) red_release_add(&signal[f * gridDim.y + blockIdx.y], 1);
-    }
 }
 
 }  // namespace flr

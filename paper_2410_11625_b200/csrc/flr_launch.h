@@ -58,12 +58,6 @@ struct LaunchCtx {
     bool capturing = false;   // stream capture: events become graph event-record nodes
     bool unsupported = false; // set by launchers compiled out of a dev build (FLR_STUB)
     bool early = false;       // FLR_FLAG_INPUTS_READY: the moment grid streams before its grid wait
-    // row wavefront across the K1 -> K2 -> K3 grids (flags zeroed per call): K2 tiles wait
-    // on per-row FIT counters, APPLY items on per-tile-row K2 counters, instead of on the
-    // completion of the whole previous grid (griddepcontrol.wait)
-    int* wave_flags = nullptr;     // workspace flag area, nullptr = off
-    const int* wave_k2 = nullptr;  // set by launch_fit when K2 signals: [n][wave_nrt]
-    int wave_nrt = 0, wave_target = 0;
     void record()
     {
         if (events && recorded < capacity) {
@@ -82,7 +76,7 @@ struct LaunchCtx {
     void end() { record(); }
 };
 
-// K1 -> K2a -> K2b -> K3 into `models` (mstride floats per block)
+// K1 -> K2 (blur + solve) into `models` (mstride floats per block)
 // A (optional): albedo [n][3][H][W]; the fit then uses Y / max(A, afloor) as its radiance
 // (demodulation fused into the moment kernel; only when fit_mod_fused() holds)
 template <int Q>
@@ -129,22 +123,6 @@ inline bool apply_mod_fused(int D, int W, const void* models, const void* G, con
            (!Dl || vec_ok(Dl, W));
 }
 
-// the fused single-kernel schedule (flr_fused.cuh); returns false when this (Q, D_fit,
-// D_out, R, alignment) combination is not compiled in, so the caller falls back to the
-// staged kernels.  `flags` = 4 * n * (By + ceil(By/4)) bytes of workspace.
-struct FusedLaunch {
-    int n, W, H, D, U, Bx, By;              // fit resolution, block size, upsample
-    const float *G, *Y, *Gout;              // fit guides, fit radiance, output-resolution guides
-    float* out;
-    double* mom;
-    float* models;                          // padded [n][By][Bx][MSTRIDE]
-    int* flags;
-    double eps_add, eps_mul;
-    Taps taps;
-};
-template <int Q>
-bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx);
-
 #define FLR_DECLARE_Q(Q)                                                                          \
     extern template void launch_fit<Q>(int, int, int, int, int, int, const float*, const float*,  \
                                        float*, double*, double*, float*, int, double, double,     \
@@ -152,7 +130,6 @@ bool launch_fused(const FusedLaunch& L, LaunchCtx& ctx);
     extern template void launch_apply<Q>(int, int, int, int, int, int, const float*, int,         \
                                          const float*, float*, LaunchCtx&, const float*,          \
                                          const float*, bool);                                     \
-    extern template bool launch_fused<Q>(const FusedLaunch&, LaunchCtx&);                      \
     extern template bool apply_mod_supported<Q>();
 FLR_DECLARE_Q(1) FLR_DECLARE_Q(2) FLR_DECLARE_Q(3) FLR_DECLARE_Q(4) FLR_DECLARE_Q(5)
 FLR_DECLARE_Q(6) FLR_DECLARE_Q(7) FLR_DECLARE_Q(8) FLR_DECLARE_Q(9) FLR_DECLARE_Q(10)

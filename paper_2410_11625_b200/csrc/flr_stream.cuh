@@ -104,8 +104,6 @@ struct FitArgs {
     CUtensorMap ty;  // radiance [n*3][H][W], box {128, 1, 3}
     double* mom;     // [n][KM][By][Bxp]
     int W, H, Bx, Bxp, By, nseg;
-    int* done;       // optional [n][By] row counters (+1 per finished item, release)
-    int gpol;        // L2 policy code (policy_by_code) of the guide reads
     CUtensorMap ta;  // albedo [n*3][H][W], box {128, 1, 3} (modulated fit only)
     float afloor;    // albedo floor of the demodulation (modulated fit only)
     int early;       // inputs ready (FLR_FLAG_INPUTS_READY): stream before the grid-dependency
@@ -126,273 +124,6 @@ __device__ __forceinline__ void fit_issue_row(const FitArgs& a, int f, int by, i
     if (MOD) tma_load_3d(dst + Q * GF + 3 * SW, &a.ta, x, y, f * 3, bar, pol_y);
 }
 
-// packed-pair layout of the FIT accumulators: d is paired over planes (2p, 2p+1)
-template <int Q>
-struct FitPack {
-    static constexpr int QP = (Q + 1) / 2;
-    __host__ __device__ static constexpr int s2_base(int i)
-    {
-        int b = 0;
-        for (int t = 0; t < i; ++t) b += QP - t / 2;
-        return b;
-    }
-    static constexpr int NS2 = s2_base(Q);
-    __host__ __device__ static constexpr int s2(int i, int p) { return s2_base(i) + p - i / 2; }  // p >= i/2
-};
-
-// FIT accumulators of one lane: fp32 sums about the block shift c, packed in pairs
-template <int Q>
-struct FitAcc {
-    using FP = FitPack<Q>;
-    static constexpr int QP = FP::QP;
-    f2 U2[QP], S2[FP::NS2], XY2[3][QP], Y2[3];
-    __device__ __forceinline__ void zero()
-    {
-#pragma unroll
-        for (int p = 0; p < QP; ++p) U2[p] = 0ull;
-#pragma unroll
-        for (int s = 0; s < FP::NS2; ++s) S2[s] = 0ull;
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-            Y2[cc] = 0ull;
-#pragma unroll
-            for (int p = 0; p < QP; ++p) XY2[cc][p] = 0ull;
-        }
-    }
-    // one pixel pair: g[j][k], y[c][k], k = 0, 1 (pixels already replaced by c when outside)
-    __device__ __forceinline__ void add_pair(const float (&g)[Q][2], const float (&yv)[3][2], const float* c)
-    {
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) Y2[cc] = add2(Y2[cc], pk2(yv[cc][0], yv[cc][1]));
-#ifndef FLR_DBG_NOCOMPUTE
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            float d[2 * QP];
-#pragma unroll
-            for (int j = 0; j < 2 * QP; ++j) d[j] = j < Q ? g[j][k] - c[j] : 0.f;
-            f2 d2[QP];
-#pragma unroll
-            for (int p = 0; p < QP; ++p) {
-                d2[p] = pk2(d[2 * p], d[2 * p + 1]);
-                U2[p] = add2(U2[p], d2[p]);
-            }
-#pragma unroll
-            for (int i = 0; i < Q; ++i)
-#pragma unroll
-                for (int p = i / 2; p < QP; ++p) S2[FP::s2(i, p)] = fma2(bc2(d[i]), d2[p], S2[FP::s2(i, p)]);
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc)
-#pragma unroll
-                for (int p = 0; p < QP; ++p) XY2[cc][p] = fma2(bc2(yv[cc][k]), d2[p], XY2[cc][p]);
-        }
-#else
-        S2[0] = add2(S2[0], pk2(g[0][0], g[Q - 1][1]));
-#endif
-    }
-    // sum over the `m`-lane groups of a block (xor shuffles)
-    __device__ __forceinline__ void combine(int m)
-    {
-#pragma unroll
-        for (int p = 0; p < QP; ++p) U2[p] = add2(U2[p], __shfl_xor_sync(0xffffffffu, U2[p], m));
-#pragma unroll
-        for (int s = 0; s < FP::NS2; ++s) S2[s] = add2(S2[s], __shfl_xor_sync(0xffffffffu, S2[s], m));
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-            Y2[cc] = add2(Y2[cc], __shfl_xor_sync(0xffffffffu, Y2[cc], m));
-#pragma unroll
-            for (int p = 0; p < QP; ++p) XY2[cc][p] = add2(XY2[cc][p], __shfl_xor_sync(0xffffffffu, XY2[cc][p], m));
-        }
-    }
-    // un-shift in fp64 (x = d + c) and store component k of block (f, by, bx) if `mine(k)`
-    template <class Mine>
-    __device__ __forceinline__ void store(double* mom, int f, int by, int bx, int By, int Bxp, double n, const float* c,
-                                          Mine mine) const
-    {
-        using Dm = Dims<Q>;
-        double u[Q], yc[3];
-#pragma unroll
-        for (int j = 0; j < Q; ++j) u[j] = (double)((j & 1) ? hi2(U2[j / 2]) : lo2(U2[j / 2]));
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) yc[cc] = (double)lo2(Y2[cc]) + (double)hi2(Y2[cc]);
-        const size_t cs = (size_t)By * Bxp;
-        double* out = mom + (size_t)f * Dm::KM * cs + (size_t)by * Bxp + bx;
-        auto put = [&](int k, double v) {
-#ifndef FLR_DBG_NOSTORE
-            if (mine(k)) out[(size_t)k * cs] = v;
-#else
-            if (v == 12345.678) out[(size_t)k * cs] = v;
-#endif
-        };
-        put(Dm::C_N, n);
-#pragma unroll
-        for (int j = 0; j < Q; ++j) put(Dm::C_U + j, fma(n, (double)c[j], u[j]));
-        // S_ij = S'_ij + c_i u'_j + c_j u'_i + n c_i c_j (compile-time (i, j): accumulators stay in registers)
-        static_for<Q>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            static_for<Q - i>([&](auto JJ) {
-                constexpr int j = i + decltype(JJ)::value;
-                const f2 sp = S2[FP::s2(i, j / 2)];
-                double v = (double)((j & 1) ? hi2(sp) : lo2(sp));
-                v = fma((double)c[i], u[j], v);
-                v = fma((double)c[j], u[i], v);
-                v = fma(n * (double)c[i], (double)c[j], v);
-                put(Dm::s_idx(i, j), v);
-            });
-        });
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) put(Dm::C_Y + cc, yc[cc]);
-#pragma unroll
-        for (int j = 0; j < Q; ++j)
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-                const f2 xp = XY2[cc][j / 2];
-                put(Dm::C_XY + j * 3 + cc, fma((double)c[j], yc[cc], (double)((j & 1) ? hi2(xp) : lo2(xp))));
-            }
-    }
-};
-
-template <int Q, int D, class Seq>
-__device__ __forceinline__ void fit_consume(Ring& r, Seq& q, const FitArgs& a, int f, int by, int sg, int lane)
-{
-    constexpr int DQ = D / 4, QP = FitPack<Q>::QP;
-    const int x0 = sg * kSeg + lane * 4;
-    const int bx = x0 / D;
-    const int lb0 = (lane / DQ) * D;  // first pixel of the lane's block within the segment
-    const int rows = min(D, a.H - by * D);
-    float c[2 * QP];
-    FitAcc<Q> acc;
-    acc.zero();
-#pragma unroll 1  // keep the row body resident in the instruction cache
-    for (int rr = 0; rr < rows; ++rr) {
-        const float* st = ring_wait(r, q, lane);
-        if (rr == 0) {
-#pragma unroll
-            for (int j = 0; j < 2 * QP; ++j) c[j] = j < Q ? st[j * kSeg + lb0] : 0.f;  // block's top-left pixel
-        }
-        // two pixel pairs per lane: 8-byte shared loads keep the live set small
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            float g[Q][2], yv[3][2];
-#pragma unroll
-            for (int j = 0; j < Q; ++j) {
-                const float2 v = reinterpret_cast<const float2*>(st + j * kSeg)[2 * lane + h];
-                g[j][0] = v.x; g[j][1] = v.y;
-            }
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const float2 v = reinterpret_cast<const float2*>(st + (Q + j) * kSeg)[2 * lane + h];
-                yv[j][0] = v.x; yv[j][1] = v.y;
-            }
-            if (h == 1) ring_release(r, q, lane);
-            // pixels beyond the image arrive as zeros: make them contribute nothing
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-                if (x0 + 2 * h + k >= a.W) {
-#pragma unroll
-                    for (int j = 0; j < Q; ++j) g[j][k] = c[j];
-                }
-            acc.add_pair(g, yv, c);
-        }
-    }
-#pragma unroll
-    for (int m = 1; m < DQ; m <<= 1) acc.combine(m);
-    if (bx >= a.Bx) return;
-    const int gi = lane % DQ;
-    acc.store(a.mom, f, by, bx, a.By, a.Bxp, (double)(min(D, a.W - bx * D) * rows), c,
-              [&](int k) { return k % DQ == gi; });
-}
-
-// ============================================================================
-// FIT without a shared-memory ring: each lane loads its pixel quad of every plane
-// straight from global memory (16-byte, L1-bypassing) one row ahead of the math, so
-// the loads of row r+1 are in flight while row r is accumulated.  No mbarriers, no
-// producer lane; all 32 lanes issue their own loads.  Requires W % 4 == 0.
-// ============================================================================
-struct FitLdgArgs {
-    const float* guides;    // [n][Q][H][W]
-    const float* radiance;  // [n][3][H][W]
-    double* mom;            // [n][KM][By][Bxp]
-    int W, H, Bx, Bxp, By, nseg;
-};
-
-template <int Q>
-__device__ __forceinline__ void fit_ldg_row(const float* G, const float* Y, size_t plane, bool active, float4 (&g)[Q],
-                                            float4 (&y)[3])
-{
-#pragma unroll
-    for (int j = 0; j < Q; ++j) {
-        if (active) {
-            asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(g[j].x), "=f"(g[j].y), "=f"(g[j].z), "=f"(g[j].w)
-                         : "l"(G + j * plane));
-        } else {
-            g[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        if (active) {
-            asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(y[j].x), "=f"(y[j].y), "=f"(y[j].z), "=f"(y[j].w)
-                         : "l"(Y + j * plane));
-        } else {
-            y[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    }
-}
-
-template <int Q, int D>
-__device__ __forceinline__ void fit_ldg_item(const FitLdgArgs& a, int f, int by, int sg, int lane)
-{
-    constexpr int DQ = D / 4, QP = FitPack<Q>::QP;
-    const int x0 = sg * kSeg + lane * 4;
-    const int bx = x0 / D;
-    const bool active = x0 < a.W;
-    const int rows = min(D, a.H - by * D);
-    const size_t plane = (size_t)a.W * a.H;
-    const size_t off = (size_t)(by * D) * a.W + x0;
-    const float* G = a.guides + (size_t)f * Q * plane + off;
-    const float* Y = a.radiance + (size_t)f * 3 * plane + off;
-    float4 gn[Q], yn[3];
-    fit_ldg_row<Q>(G, Y, plane, active, gn, yn);
-    float c[2 * QP];
-    const int lead = lane & ~(DQ - 1);  // the lane holding the block's top-left pixel
-#pragma unroll
-    for (int j = 0; j < 2 * QP; ++j) c[j] = j < Q ? __shfl_sync(0xffffffffu, gn[j < Q ? j : 0].x, lead) : 0.f;
-    FitAcc<Q> acc;
-    acc.zero();
-#pragma unroll 1
-    for (int rr = 0; rr < rows; ++rr) {
-        float4 gc[Q], yc[3];
-#pragma unroll
-        for (int j = 0; j < Q; ++j) gc[j] = gn[j];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) yc[j] = yn[j];
-        if (rr + 1 < rows) fit_ldg_row<Q>(G + (size_t)(rr + 1) * a.W, Y + (size_t)(rr + 1) * a.W, plane, active, gn, yn);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            float g[Q][2], yv[3][2];
-#pragma unroll
-            for (int j = 0; j < Q; ++j) {
-                g[j][0] = active ? (h ? gc[j].z : gc[j].x) : c[j];
-                g[j][1] = active ? (h ? gc[j].w : gc[j].y) : c[j];
-            }
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                yv[j][0] = h ? yc[j].z : yc[j].x;
-                yv[j][1] = h ? yc[j].w : yc[j].y;
-            }
-            acc.add_pair(g, yv, c);
-        }
-    }
-#pragma unroll
-    for (int m = 1; m < DQ; m <<= 1) acc.combine(m);
-    if (bx >= a.Bx) return;
-    const int gi = lane % DQ;
-    acc.store(a.mom, f, by, bx, a.By, a.Bxp, (double)(min(D, a.W - bx * D) * rows), c,
-              [&](int k) { return k % DQ == gi; });
-}
-
 // ============================================================================
 // APPLY item: frame f, band j (output rows [jD - D/2, jD + D/2) inside the image),
 // segment sg (output pixels [128 sg, 128 sg + 128)).  Every row of band j lies between
@@ -405,8 +136,6 @@ struct ApplyArgs {
     float* out;           // [n][3][H][W]
     int W, H, D, Bx, By, nseg, nband;
     int nsub;  // sub-bands per band (D % nsub == 0): more, smaller APPLY items for one frame
-    const int* ready;  // optional [n][nrt] K2 tile-row counters (complete at ready_target)
-    int ready_target, nrt, ready_ty;  // ready_ty: block rows per counter
     int reverse;  // walk each frame's items bottom-up (the rows the fit read last come first)
     CUtensorMap ta, td;  // albedo, direct [n*3][H][W], box {128, 1, 3} (modulated apply only)
     int has_direct;      // modulated apply: 0 = no direct-light planes (treated as zero)

@@ -1,7 +1,7 @@
 // flr_tiles.cuh -- tiled sm_100a kernels of the staged FLR schedule:
 //   K1 k_fit_moments : outer products + strided box downsample
-//   K2 k_blur_solve  : separable Gaussian blur of the moment field + per-block solve
-//
+//   K2 k_blur_rows + k_solve_rows / k_solve: row-strip blur of the moment field, then the
+//                      per-block solve
 //   K4 k_apply_tile  : bilinear model blend + application
 // Full-resolution planes are streamed once per pass with 16-byte loads; all
 // intermediates live at block resolution.
@@ -246,260 +246,8 @@ __global__ void __launch_bounds__(FitGeom<D>::THREADS) k_fit_moments(int W, int 
     }
 }
 
-// ===========================================================================
-// K2: blur + solve.  One CTA = TX x TY output blocks (one thread each).  For each
-// group of G moment components, ONE 3-D TMA load brings the (TY+2R) x (TX+2R) halo
-// of the pitched fp64 moment field into shared memory (out-of-grid blocks read as
-// zero = the zero padding of R3; double-buffered on two mbarriers); a vertical
-// pass -> TY x (TX+2R) and a horizontal pass -> registers (P:299-309, P:316,
-// P:334); then the appendix solve per thread (flr_solve.cuh).  R <= kTileMaxR.
-// ===========================================================================
-constexpr int kTileTX = 32, kTileTY = 4, kTileG = 12, kTileMaxR = 8;
-
-// TMA box starts must be 16-byte aligned: the x halo is rounded up to an even count
-__host__ __device__ constexpr int halo_x(int R) { return kTileTX + 2 * ((R + 1) & ~1); }
-
-__host__ __device__ constexpr int tile_g(int R) { return R <= 3 ? kTileG : 8; }
-inline size_t blur_solve_smem_bytes(int R)
-{
-    const int HX = halo_x(R), HY = kTileTY + 2 * R, G = tile_g(R);
-    return (size_t)(2 * G * HY * HX + G * kTileTY * HX) * sizeof(double) + 2 * sizeof(uint64_t);
-}
-template <int R>
-struct TileGeom;
-
-// synchronisation of the group of threads that runs a blur+solve tile
-struct CtaSync {
-    __device__ void sync() const { __syncthreads(); }
-};
-struct NamedSync {  // named barrier over `n` threads (a warp-specialised sub-group of the CTA)
-    int id, n;
-    __device__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-};
-
-template <int R>
-struct TileGeom {
-    static constexpr int RE = (R + 1) & ~1;  // x halo (even: 16-byte aligned TMA box start)
-    static constexpr int HX = kTileTX + 2 * RE, HY = kTileTY + 2 * R;
-    static constexpr int G = R <= 3 ? kTileG : 8;  // components per halo box
-    static constexpr int HALO = G * HY * HX;  // doubles per halo buffer
-    static constexpr int VB = G * kTileTY * HX;
-    static constexpr size_t SMEM = (size_t)(2 * HALO + VB) * sizeof(double);
-};
-
-// One TX x TY tile of output blocks, run by NT = TX*TY threads (tid = 0..NT-1) that
-// share `sm` (TileGeom<R>::SMEM bytes) and two mbarriers `bar`; `use[b]` counts the
-// completed uses of bar[b] (phase parity), identical in every thread of the group.
-template <int Q, int R, class Sync>
-__device__ __forceinline__ void blur_solve_tile(const CUtensorMap* tm, int f, int bx0, int by0, int Bx, int By,
-                                                float* __restrict__ models, int mstride, double eps_add,
-                                                double eps_mul, const Taps& t, double* sm, uint64_t* bar,
-                                                unsigned (&use)[2], int tid, Sync grp_sync)
-{
-    using Dm = Dims<Q>;
-    using TG = TileGeom<R>;
-    constexpr int KM = Dm::KM, GG = TG::G, NG = (KM + GG - 1) / GG;
-    constexpr int TX = kTileTX, TY = kTileTY, NT = TX * TY;
-    constexpr int RE = TG::RE, HX = TG::HX, HY = TG::HY, NTAP = 2 * R + 1;
-    constexpr unsigned BOX_BYTES = TG::HALO * sizeof(double);
-    double* halo[2] = {sm, sm + TG::HALO};
-    double* vb = sm + 2 * TG::HALO;
-    const int tx = tid % TX, ty = tid / TX;
-    double g[NTAP];
-#pragma unroll
-    for (int d = 0; d < NTAP; ++d) g[d] = t.g[d];
-    auto issue = [&](int grp) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the buffer
-        mbar_arrive_expect_tx(&bar[grp & 1], BOX_BYTES);
-        tma_load_3d(halo[grp & 1], tm, bx0 - RE, by0 - R, f * KM + grp * GG, &bar[grp & 1], policy_evict_normal());
-    };
-#ifdef FLR_DBG_TIMES
-    long long tstamp[2 * NG + 3];
-    tstamp[0] = clock64();
-#endif
-    if (tid == 0) issue(0);
-
-    double blur[KM];
-#pragma unroll
-    for (int grp = 0; grp < NG; ++grp) {
-        if (tid == 0 && grp + 1 < NG) issue(grp + 1);  // buffer (grp+1)&1 was released by the last sync
-        mbar_wait(&bar[grp & 1], use[grp & 1] & 1);
-#ifdef FLR_DBG_TIMES
-        tstamp[1 + 2 * grp] = clock64();
-#endif
-        ++use[grp & 1];
-        const double* h = halo[grp & 1];
-        // vertical pass: one thread per (component, halo column) pair of columns, TY outputs
-        // each from HY loads; symmetric taps g_d = g_-d halve the dependent chain
-        for (int col = tid; col < GG * HX; col += 2 * NT) {
-            const int col2 = col + NT;
-            const bool two = col2 < GG * HX;
-            const int gi = col / HX, cc = col - gi * HX;
-            const int gi2 = two ? col2 / HX : gi, cc2 = two ? col2 - gi2 * HX : cc;
-            const double* src = h + gi * HY * HX + cc;
-            const double* src2 = h + gi2 * HY * HX + cc2;
-            double v[HY], w[HY];
-#pragma unroll
-            for (int r = 0; r < HY; ++r) {
-                v[r] = src[r * HX];
-                w[r] = src2[r * HX];
-            }
-#pragma unroll
-            for (int r = 0; r < TY; ++r) {
-                double a = g[R] * v[r + R], b = g[R] * w[r + R];
-#pragma unroll
-                for (int d = 1; d <= R; ++d) {
-                    a = fma(g[R + d], v[r + R - d] + v[r + R + d], a);
-                    b = fma(g[R + d], w[r + R - d] + w[r + R + d], b);
-                }
-                vb[(gi * TY + r) * HX + cc] = a;
-                if (two) vb[(gi2 * TY + r) * HX + cc2] = b;
-            }
-        }
-        grp_sync.sync();
-        // horizontal pass: one thread per output block, GG independent chains
-#pragma unroll
-        for (int gi = 0; gi < GG; ++gi) {
-            const int k = grp * GG + gi;
-            if (k < KM) {
-                const double* src = vb + (gi * TY + ty) * HX + tx + RE;
-                double acc = g[R] * src[0];
-#pragma unroll
-                for (int d = 1; d <= R; ++d) acc = fma(g[R + d], src[-d] + src[d], acc);
-                blur[k] = acc;
-            }
-        }
-        grp_sync.sync();
-#ifdef FLR_DBG_TIMES
-        tstamp[2 + 2 * grp] = clock64();
-#endif
-    }
-    const int bx = bx0 + tx, by = by0 + ty;
-#ifdef FLR_DBG_TIMES
-    if (bx >= Bx || by >= By) return;
-    solve_block<Q>([&](int k) { return blur[k]; }, eps_add, eps_mul,
-                   models + ((size_t)(f * By + by) * Bx + bx) * mstride);
-    tstamp[2 * NG + 1] = clock64();
-    if (tid == 0 && bx0 == (Bx >= 96 ? 64 : 0) && by0 == (By >= 96 ? 64 : 0)) {
-        extern __device__ long long g_flr_dbg_times[64];
-        for (int i = 0; i <= 2 * NG + 1; ++i) g_flr_dbg_times[i] = tstamp[i] - tstamp[0];
-        g_flr_dbg_times[63] = 2 * NG + 2;
-    }
-    return;
-#endif
-    if (bx >= Bx || by >= By) return;
-#ifdef FLR_DBG_BLUR_NOSOLVE
-    models[((size_t)(f * By + by) * Bx + bx) * mstride] = (float)(blur[0] + blur[KM - 1]);
-#else
-    solve_block<Q>([&](int k) { return blur[k]; }, eps_add, eps_mul,
-                   models + ((size_t)(f * By + by) * Bx + bx) * mstride);
-#endif
-}
-
-template <int Q, int R>
-__global__ void __launch_bounds__(kTileTX* kTileTY) k_blur_solve(const __grid_constant__ CUtensorMap tm, int Bx, int By,
-                                                                float* __restrict__ models, int mstride,
-                                                                double eps_add, double eps_mul,
-                                                                const __grid_constant__ Taps t)
-{
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    double* sm = reinterpret_cast<double*>(smem_raw);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + TileGeom<R>::SMEM);
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    pdl_wait();  // the moment field comes from the previous grid
-    pdl_trigger();  // dependents launch only once we are past our own wait
-    __syncthreads();
-    unsigned use[2] = {0, 0};
-    blur_solve_tile<Q, R>(&tm, blockIdx.z, blockIdx.x * kTileTX, blockIdx.y * kTileTY, Bx, By, models, mstride,
-                          eps_add, eps_mul, t, sm, bar, use, threadIdx.x, CtaSync{});
-}
-
-// ===========================================================================
-// K2' (high-occupancy split of K2): k_blur blurs GB components of a BTX x BTY tile of
-// the moment field per CTA (TMA halo box, vertical then horizontal pass, fp64) and
-// writes the blurred field; k_solve runs the appendix solve, one thread per block.
-// Many small CTAs per SM keep the fp64 pipe busy where the fused tile kernel is
-// latency-bound on a few register-heavy threads.
-// ===========================================================================
-constexpr int kBlurTX = 32, kBlurTY = 8, kBlurG = 6;
-
-template <int R>
-struct BlurGeom {
-    static constexpr int RE = (R + 1) & ~1;
-    static constexpr int HX = kBlurTX + 2 * RE, HY = kBlurTY + 2 * R;
-    static constexpr int HALO = kBlurG * HY * HX;      // doubles
-    static constexpr int VB = kBlurG * kBlurTY * HX;   // doubles
-    static constexpr size_t SMEM = (size_t)(HALO + VB) * sizeof(double) + sizeof(uint64_t);
-};
-__host__ __device__ constexpr int blur_halo_x(int R) { return kBlurTX + 2 * ((R + 1) & ~1); }
-
-// grid: (ceil(Bx/BTX), ceil(By/BTY), n * ceil(KM/GB)); out: blurred field, same pitched layout
-template <int Q, int R>
-__global__ void __launch_bounds__(256) k_blur(const __grid_constant__ CUtensorMap tm, int Bx, int Bxp, int By,
-                                             double* __restrict__ blurred, const __grid_constant__ Taps t)
-{
-    using BG = BlurGeom<R>;
-    constexpr int KM = Dims<Q>::KM, NGRP = (KM + kBlurG - 1) / kBlurG;
-    constexpr int HX = BG::HX, HY = BG::HY, RE = BG::RE, NTAP = 2 * R + 1, TY = kBlurTY, TX = kBlurTX;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    double* halo = reinterpret_cast<double*>(smem_raw);
-    double* vb = halo + BG::HALO;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(vb + BG::VB);
-    const int f = blockIdx.z / NGRP, grp = blockIdx.z - f * NGRP;
-    const int bx0 = blockIdx.x * TX, by0 = blockIdx.y * TY, k0 = grp * kBlurG;
-    pdl_wait();  // the moment field comes from the previous grid
-    pdl_trigger();  // dependents launch only once we are past our own wait
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        fence_mbar_init();
-        mbar_arrive_expect_tx(bar, BG::HALO * sizeof(double));
-        tma_load_3d(halo, &tm, bx0 - RE, by0 - R, f * KM + k0, bar, policy_evict_normal());
-    }
-    double g[NTAP];
-#pragma unroll
-    for (int d = 0; d < NTAP; ++d) g[d] = t.g[d];
-    __syncthreads();
-    mbar_wait(bar, 0);
-    // vertical pass: one thread per (component, halo column): TY outputs, TY independent chains
-    for (int col = threadIdx.x; col < kBlurG * HX; col += blockDim.x) {
-        const int gi = col / HX, cc = col - gi * HX;
-        const double* src = halo + gi * HY * HX + cc;
-        double v[HY];
-#pragma unroll
-        for (int r = 0; r < HY; ++r) v[r] = src[r * HX];
-#pragma unroll
-        for (int r = 0; r < TY; ++r) {
-            double acc = g[R] * v[r + R];
-#pragma unroll
-            for (int d = 1; d <= R; ++d) acc = fma(g[R + d], v[r + R - d] + v[r + R + d], acc);
-            vb[(gi * TY + r) * HX + cc] = acc;
-        }
-    }
-    __syncthreads();
-    // horizontal pass: one thread per (component, row, 4 consecutive blocks)
-    const size_t cs = (size_t)By * Bxp;
-    for (int u = threadIdx.x; u < kBlurG * TY * (TX / 4); u += blockDim.x) {
-        const int x4 = u % (TX / 4), rr = (u / (TX / 4)) % TY, gi = u / ((TX / 4) * TY);
-        const int k = k0 + gi, by = by0 + rr;
-        if (k >= KM || by >= By) continue;
-        const double* src = vb + (gi * TY + rr) * HX + 4 * x4 + (RE - R);
-        double v[NTAP + 3];
-#pragma unroll
-        for (int i = 0; i < NTAP + 3; ++i) v[i] = src[i];
-        double* dst = blurred + ((size_t)f * KM + k) * cs + (size_t)by * Bxp + bx0 + 4 * x4;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            double acc = g[R] * v[e + R];
-#pragma unroll
-            for (int d = 1; d <= R; ++d) acc = fma(g[R + d], v[e + R - d] + v[e + R + d], acc);
-            if (bx0 + 4 * x4 + e < Bx) dst[e] = acc;
-        }
-    }
-}
+// blur half-width (blocks) handled by the tiled K2 kernels (flr_k2.cuh, k_blur_rows)
+constexpr int kTileMaxR = 8;
 
 // ===========================================================================
 // K2a (row-strip blur): the separable Gaussian of P:334 over a strip of kRowsCH block

@@ -44,6 +44,34 @@ def gather_rows(row, device=None):
     return [t.tolist()]
 
 
+def per_frame_checksums(out):
+    """[n, 3] float64 rows [sum, max |x|, all finite] of each frame of an [n, ...] result."""
+    o = out.double().reshape(out.shape[0], -1)
+    return torch.stack([o.sum(1), o.abs().amax(1), torch.isfinite(o).all(1).double()], 1)
+
+
+def gather_frame_checksums(rows, lo: int, n_total: int, device=None):
+    """Assemble every rank's per-frame checksum rows ([hi - lo, 3], frames [lo, hi) of the
+    global batch, as shard_range hands them out) into one [n_total, 3] float64 tensor in
+    global frame order, on every rank (one all_gather of fixed-size padded blocks)."""
+    rows = torch.as_tensor(rows, dtype=torch.float64, device=device).reshape(-1, 3)
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    if world == 1:
+        return rows.cpu()
+    cap = -(-n_total // world)  # largest shard
+    buf = torch.full((cap + 1, 3), float("nan"), dtype=torch.float64, device=device)
+    buf[0, 0], buf[0, 1] = float(lo), float(rows.shape[0])
+    buf[1:1 + rows.shape[0]] = rows
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    full = torch.full((n_total, 3), float("nan"), dtype=torch.float64)
+    for p in parts:
+        p = p.cpu()
+        a, m = int(p[0, 0]), int(p[0, 1])
+        full[a:a + m] = p[1:1 + m]
+    return full
+
+
 def output_checksum(out) -> list:
     """[sum, max |x|, all finite] of a result tensor, in float64."""
     o = out.double()

@@ -61,7 +61,7 @@ int main(int argc, char** argv)
         float tt = 0;
         for (int rep = 0; rep < 2000; ++rep) {
             if (rep == 1990) cudaEventRecord(e[0]);
-            k_blur_solve_tile<Q, R><<<gt, kK2Threads, KG::SMEM>>>(tmk, Bx, By, models, 1e-5, 1e-4, t, nullptr, 0, nullptr, 1);
+            k_blur_solve_tile<Q, R><<<gt, kK2Threads, KG::SMEM>>>(tmk, Bx, By, models, Dims<Q>::MSTRIDE, 1e-5, 1e-4, t);
         }
         cudaEventRecord(e[1]);
         cudaEventSynchronize(e[1]);
