@@ -72,8 +72,12 @@ typedef enum {
 typedef enum {
     FLR_VARIANT_AUTO = 0,   /* the fastest schedule for the shape (currently STAGED) */
     FLR_VARIANT_STAGED = 1, /* moments -> blur+solve -> apply, one launch each */
-    FLR_VARIANT_FUSED = 2   /* one persistent warp-specialised kernel (row wavefront);
-                               FLR_ERR_UNSUPPORTED when not compiled for the shape */
+    FLR_VARIANT_FUSED = 2   /* one persistent kernel per call: every CTA claims FIT chunks,
+                               blur+solve tiles and APPLY chunks from workspace queues as
+                               their inputs complete (row wavefront; bitwise equal to STAGED).
+                               Compiled for Q in {4, 8}, block in {4, 8}, radius in {3, 5},
+                               output block a multiple of 8, 16-byte aligned planes with
+                               W % 4 == 0; FLR_ERR_UNSUPPORTED otherwise */
 } flr_variant;
 
 /* Per-block solver. */

@@ -26,6 +26,8 @@ QS = range(1, 16)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
                   "-I", os.path.join(ROOT, "include")]
+# developer builds only: extra nvcc defines, e.g. FLR_DEFS="-DFLR_WATCHDOG" (hang diagnostics)
+NVFLAGS += os.environ.get("FLR_DEFS", "").split()
 
 
 def _nvcc():

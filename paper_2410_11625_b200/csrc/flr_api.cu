@@ -49,7 +49,7 @@ int effective_radius(const flr_params* p)
 }
 
 struct Layout {
-    size_t raw, mom, hb, models, total;
+    size_t raw, mom, hb, models, flags, total;
 };
 
 // workspace: raw fp32 moments | fp64 un-shifted moments | fp64 x-blurred | padded models
@@ -67,6 +67,8 @@ Layout layout(int n, int Q, int Bx, int By)
     off += align256(nbp * km_of(Q) * sizeof(double));
     L.models = off;
     off += align256(nb * mstride_of(Q) * sizeof(float));
+    L.flags = off;  // task-queue heads + row counters of the wave schedule (zeroed per call)
+    off += align256(sizeof(int) * (size_t)wave_flags_ints(n, By));
     L.total = off;
     return L;
 }
@@ -307,6 +309,21 @@ flr_status denoise_upsample_impl(int32_t n, int32_t Q, int32_t W_lo, int32_t H_l
     float* models = (float*)((char*)workspace + L.models);
     const int ms = mstride_of(Q);
     LaunchCtx ctx = make_ctx(stream, trace);
+    // FUSED: the one-kernel wave schedule (flr_wave.cuh).  AUTO stays on the staged kernels:
+    // on B200 the wave schedule is correct (bitwise equal) but slower
+    if (p->variant == FLR_VARIANT_FUSED && !hg) {
+        WaveLaunch W;
+        W.n = n, W.W = W_lo, W.H = H_lo, W.D = D, W.U = p->upsample, W.Bx = Bx, W.By = By;
+        W.G = guides_lo, W.Y = radiance_lo, W.Gout = guides_hi, W.out = out;
+        W.mom = (double*)((char*)workspace + L.mom);
+        W.models = models;
+        W.flags = (int*)((char*)workspace + L.flags);
+        W.eps_add = p->eps_add, W.eps_mul = solver_eps_mul(p);
+        W.taps = make_taps(p->sigma / ((double)D * p->upsample), effective_radius(p));
+        bool done = false;
+        FLR_DISPATCH_Q(Q, (done = launch_wave<QQ>(W, ctx)));
+        if (done) return finish(ctx, trace);
+    }
     if (p->variant == FLR_VARIANT_FUSED) return FLR_ERR_UNSUPPORTED;
     const int Dout = D * p->upsample;
     if (hg && (!half_guides_fit_ok(D, W_lo, guides_lo, radiance_lo) ||

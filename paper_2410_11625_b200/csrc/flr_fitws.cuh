@@ -37,19 +37,28 @@ static_assert(kFS == 128 || kFS == 64, "fit segment: 64 or 128 pixels");
 
 template <int Q, bool MOD = false, bool HG = false>
 struct FitWsCfg {
-    // floats per stage (one pixel row): Q guide planes (fp32, or fp16 when HG), 3 radiance
+    // floats per pixel row of a stage: Q guide planes (fp32, or fp16 when HG), 3 radiance
     // planes (+ 3 albedo planes)
-    static constexpr int GF = HG ? kFS / 2 : kFS;  // floats per guide plane
-    static constexpr int STG = Q * GF + (3 + (MOD ? 3 : 0)) * kFS;
-    // as many stages (<= kFitWsS) as fit in 227 KB with 7 consumers
+    static constexpr int GF = HG ? kFS / 2 : kFS;  // floats per guide plane row
+    static constexpr int ROWF = Q * GF + (3 + (MOD ? 3 : 0)) * kFS;
+    // A stage holds RB pixel rows: one TMA box {128, RB, planes} per tensor.  The producer
+    // warp's issue rate, not HBM, limits one SM at one row per box (measured ~50 GB/s per
+    // SM, tools/t_tma_rate.cu); two rows per box double it.  RB = 2 with 2 stages per
+    // consumer when that fits in 227 KB, else single rows with up to kFitWsS stages.
+    static constexpr bool TWO = (size_t)kFitWsNC * 2 * 2 * ROWF * 4 + 4096 <= 232448;
+    static constexpr int RB = TWO ? 2 : 1;
+    static constexpr int STG = RB * ROWF;  // floats per stage
     static constexpr int fit_stages(int s)
     {
         return (s <= 2 || (size_t)kFitWsNC * s * STG * 4 + 4096 <= 232448) ? s : fit_stages(s - 1);
     }
-    static constexpr int NC = kFitWsNC, S = fit_stages(kFitWsS), THREADS = (NC + 1) * 32;
+    static constexpr int NC = kFitWsNC, S = TWO ? 2 : fit_stages(kFitWsS), THREADS = (NC + 1) * 32;
     static constexpr size_t BAR_OFF = (size_t)NC * S * STG * sizeof(float);
     static constexpr size_t SMEM = BAR_OFF + 2 * NC * S * sizeof(uint64_t);
     static_assert(SMEM <= 232448, "fit pipeline exceeds 227 KB of shared memory");
+    // offsets (floats) inside a stage: guide plane j / radiance plane c, row r of the stage
+    __host__ __device__ static constexpr int g_off(int j, int r) { return (j * RB + r) * GF; }
+    __host__ __device__ static constexpr int y_off(int c, int r) { return Q * RB * GF + (c * RB + r) * kFS; }
 };
 
 // per-lane accumulators of one item, pixel-pair packed
@@ -97,63 +106,130 @@ __device__ __forceinline__ void fold_pairs(const f2 (&in)[N], float (&out)[N], i
         for (int k = 0; k < N; ++k) out[k] += __shfl_xor_sync(0xffffffffu, out[k], m);
 }
 
-// the rows of one item for one consumer warp (k: rows consumed so far by this warp)
+// the rows of one item for one consumer warp (k: stages consumed so far by this warp)
 template <int Q, int D, bool EDGE, bool MOD, bool HG>
 __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], const float* ring, uint64_t* full,
                                             uint64_t* empty, int& k, int rows, int lane, int lb0, int x0, int W,
                                             float afloor)
 {
     using C = FitWsCfg<Q, MOD, HG>;
-    constexpr int S = C::S, STG = C::STG, GF = C::GF, RO = Q * GF;  // RO: radiance offset (floats)
+    constexpr int S = C::S, STG = C::STG, RB = C::RB;
     {  // the block shift c = its top-left pixel (first row of the item)
         mbar_wait(&full[k % S], (k / S) & 1);
         const float* st = ring + (k % S) * STG;
 #pragma unroll
         for (int j = 0; j < Q; ++j)
-            cs[j] = HG ? __half2float(reinterpret_cast<const __half*>(st + j * GF)[lb0]) : st[j * kFS + lb0];
+            cs[j] = HG ? __half2float(reinterpret_cast<const __half*>(st + C::g_off(j, 0))[lb0]) : st[C::g_off(j, 0) + lb0];
     }
 #pragma unroll 1  // keep the row body resident in the instruction cache
-    for (int rr = 0; rr < rows; ++rr, ++k) {
+    for (int r0 = 0; r0 < rows; r0 += RB, ++k) {
         const int slot = k % S;
         mbar_wait(&full[slot], (k / S) & 1);
         const float* st = ring + slot * STG;
 #pragma unroll
-        for (int h = 0; h < kNH; ++h) {
-            f2 d[Q], y[3];
+        for (int r = 0; r < RB; ++r) {
+            if (RB > 1 && r0 + r >= rows) break;  // odd row count at the bottom edge
 #pragma unroll
-            for (int j = 0; j < Q; ++j) {
-                if (HG) {  // fp16 guide pair -> fp32 (exact)
-                    const float2 v = __half22float2(reinterpret_cast<const __half2*>(st + j * GF)[kNH * lane + h]);
-                    d[j] = pk2(v.x, v.y);
-                } else {
-                    d[j] = reinterpret_cast<const f2*>(st + j * kFS)[kNH * lane + h];
+            for (int h = 0; h < kNH; ++h) {
+                f2 d[Q], y[3];
+#pragma unroll
+                for (int j = 0; j < Q; ++j) {
+                    if (HG) {  // fp16 guide pair -> fp32 (exact)
+                        const float2 v =
+                            __half22float2(reinterpret_cast<const __half2*>(st + C::g_off(j, r))[kNH * lane + h]);
+                        d[j] = pk2(v.x, v.y);
+                    } else {
+                        d[j] = reinterpret_cast<const f2*>(st + C::g_off(j, r))[kNH * lane + h];
+                    }
                 }
-            }
 #pragma unroll
-            for (int c = 0; c < 3; ++c) y[c] = reinterpret_cast<const f2*>(st + RO + c * kFS)[kNH * lane + h];
-            if (MOD) {  // demodulation y = radiance / max(albedo, floor) (R20)
+                for (int c = 0; c < 3; ++c) y[c] = reinterpret_cast<const f2*>(st + C::y_off(c, r))[kNH * lane + h];
+                if (MOD) {  // demodulation y = radiance / max(albedo, floor) (R20)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const f2 al = reinterpret_cast<const f2*>(st + RO + (3 + c) * kFS)[kNH * lane + h];
-                    y[c] = pk2(lo2(y[c]) * __frcp_rn(fmaxf(lo2(al), afloor)),
-                               hi2(y[c]) * __frcp_rn(fmaxf(hi2(al), afloor)));
+                    for (int c = 0; c < 3; ++c) {
+                        const f2 al = reinterpret_cast<const f2*>(st + C::y_off(3 + c, r))[kNH * lane + h];
+                        y[c] = pk2(lo2(y[c]) * __frcp_rn(fmaxf(lo2(al), afloor)),
+                                   hi2(y[c]) * __frcp_rn(fmaxf(hi2(al), afloor)));
+                    }
                 }
-            }
 #pragma unroll
-            for (int j = 0; j < Q; ++j) d[j] = sub2(d[j], bc2(cs[j]));
-            if (EDGE) {  // pixels past the image arrive as zeros: make them contribute nothing
-                const bool in0 = x0 + 2 * h < W, in1 = x0 + 2 * h + 1 < W;
+                for (int j = 0; j < Q; ++j) d[j] = sub2(d[j], bc2(cs[j]));
+                if (EDGE) {  // pixels past the image arrive as zeros: make them contribute nothing
+                    const bool in0 = x0 + 2 * h < W, in1 = x0 + 2 * h + 1 < W;
 #pragma unroll
-                for (int j = 0; j < Q; ++j) d[j] = pk2(in0 ? lo2(d[j]) : 0.f, in1 ? hi2(d[j]) : 0.f);
-            }
+                    for (int j = 0; j < Q; ++j) d[j] = pk2(in0 ? lo2(d[j]) : 0.f, in1 ? hi2(d[j]) : 0.f);
+                }
 #ifndef FLR_FITWS_NOCOMPUTE
-            acc.add(d, y);
+                acc.add(d, y);
 #else
-            if (lo2(d[0]) == 12345.f) acc.add(d, y);  // timing experiment: stream without accumulating
+                if (lo2(d[0]) == 12345.f) acc.add(d, y);  // timing experiment: stream without accumulating
 #endif
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);  // values are in registers: free the stage
+    }
+}
+
+// One FIT item (frame f, block row by, segment sg; item index `it`) for one consumer warp:
+// its rows from the warp's ring (k: stages consumed so far), then the epilogue -- fold the
+// pair halves and the lanes of a block, un-shift exactly to fp64 and store the moments.
+// `waited`: the grid-dependency wait has run (in early mode it runs before the first store).
+template <int Q, int D, bool MOD, bool HG>
+__device__ __forceinline__ void fit_consume_item(const FitArgs& a, int it, int per_frame, const float* ring,
+                                                 uint64_t* full, uint64_t* empty, int& k, int lane, bool& waited)
+{
+    using Dm = Dims<Q>;
+    constexpr int DQ = D / kPPL;  // lanes per block
+    const int f = it / per_frame, rem = it - f * per_frame, by = rem / a.nseg, sg = rem - by * a.nseg;
+    const int rows = min(D, a.H - by * D);
+    const int x0 = sg * kFS + lane * kPPL, bx = x0 / D, lb0 = (lane / DQ) * D;
+    float cs[Q];
+    FitAccPix<Q> acc;
+    acc.zero();
+    if (sg * kFS + kFS > a.W)  // segment reaches past the image
+        fit_ws_rows<Q, D, true, MOD, HG>(acc, cs, ring, full, empty, k, rows, lane, lb0, x0, a.W, a.afloor);
+    else
+        fit_ws_rows<Q, D, false, MOD, HG>(acc, cs, ring, full, empty, k, rows, lane, lb0, x0, a.W, a.afloor);
+    // epilogue: fold, then un-shift to fp64 and store (lanes of a block split the components)
+    float u[Q], sv[Dm::NS], yc[3], xy[3 * Q];
+    fold_pairs(acc.U, u, DQ);
+    fold_pairs(acc.S, sv, DQ);
+    fold_pairs(acc.Y, yc, DQ);
+    fold_pairs(acc.XY, xy, DQ);
+    if (!waited) {
+        pdl_wait();
+        waited = true;
+    }
+    if (bx < a.Bx) {
+        const int gi = lane % DQ;
+        const double nn = (double)(min(D, a.W - bx * D) * rows);
+        const size_t cst = (size_t)a.By * a.Bxp;
+        double* out = a.mom + (size_t)f * Dm::KM * cst + (size_t)by * a.Bxp + bx;
+        auto put = [&](int kk, double v) {
+            if (kk % DQ == gi) out[(size_t)kk * cst] = v;
+        };
+        put(Dm::C_N, nn);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) put(Dm::C_U + j, fma(nn, (double)cs[j], (double)u[j]));
+        // S_ij = S'_ij + c_i u'_j + c_j u'_i + n c_i c_j
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+            for (int j = i; j < Q; ++j) {
+                double v = (double)sv[Dm::s_idx(i, j) - Dm::C_S];
+                v = fma((double)cs[i], (double)u[j], v);
+                v = fma((double)cs[j], (double)u[i], v);
+                v = fma(nn * (double)cs[i], (double)cs[j], v);
+                put(Dm::s_idx(i, j), v);
+            }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) put(Dm::C_Y + c, (double)yc[c]);
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                put(Dm::C_XY + j * 3 + c, fma((double)cs[j], (double)yc[c], (double)xy[j * 3 + c]));
     }
 }
 
@@ -161,9 +237,8 @@ template <int Q, int D, bool MOD = false, bool HG = false>
 __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(const __grid_constant__ FitArgs a, int n)
 {
     using C = FitWsCfg<Q, MOD, HG>;
-    using Dm = Dims<Q>;
     if (threadIdx.x == 0) FLR_TL(0, 0);
-    constexpr int NC = C::NC, S = C::S, STG = C::STG, DQ = D / kPPL;  // DQ: lanes per block
+    constexpr int NC = C::NC, S = C::S, STG = C::STG;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     float* stages = reinterpret_cast<float*>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF);
@@ -213,10 +288,10 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
             const int slot = k % S;
             if (it < nitems && (k < S || mbar_test_wait(&empty[c * S + slot], ((k / S) - 1) & 1))) {
                 ws_proxy_fence();
-                fit_issue_row<Q, D, MOD, HG, kFS>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG, &full[c * S + slot],
-                                    pg, py);
+                fit_issue_row<Q, D, MOD, HG, kFS, C::RB>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG,
+                                                         &full[c * S + slot], pg, py);
                 ++k;
-                if (++row == rows) {
+                if ((row += C::RB) >= rows) {
                     row = 0;
                     it += GW;
                     decode();
@@ -233,62 +308,10 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     // ---------------- consumer warp ----------------
     const int w = warp;
     float* ring = stages + (size_t)w * S * STG;
-    int k = 0;  // rows consumed
+    int k = 0;  // stages consumed
     bool waited = !a.early;  // past the grid-dependency wait (early mode: before the first store)
-    for (int it = blockIdx.x * NC + w; it < nitems; it += GW) {
-        const int f = it / per_frame, rem = it - f * per_frame, by = rem / a.nseg, sg = rem - by * a.nseg;
-        const int rows = min(D, a.H - by * D);
-        const int x0 = sg * kFS + lane * kPPL, bx = x0 / D, lb0 = (lane / DQ) * D;
-        float cs[Q];
-        FitAccPix<Q> acc;
-        acc.zero();
-        if (sg * kFS + kFS > a.W)  // segment reaches past the image
-            fit_ws_rows<Q, D, true, MOD, HG>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
-                                         a.afloor);
-        else
-            fit_ws_rows<Q, D, false, MOD, HG>(acc, cs, ring, full + w * S, empty + w * S, k, rows, lane, lb0, x0, a.W,
-                                          a.afloor);
-        // epilogue: fold, then un-shift to fp64 and store (lanes of a block split the components)
-        float u[Q], sv[Dm::NS], yc[3], xy[3 * Q];
-        fold_pairs(acc.U, u, DQ);
-        fold_pairs(acc.S, sv, DQ);
-        fold_pairs(acc.Y, yc, DQ);
-        fold_pairs(acc.XY, xy, DQ);
-        if (!waited) {
-            pdl_wait();
-            waited = true;
-        }
-        if (bx < a.Bx) {
-        const int gi = lane % DQ;
-        const double nn = (double)(min(D, a.W - bx * D) * rows);
-        const size_t cst = (size_t)a.By * a.Bxp;
-        double* out = a.mom + (size_t)f * Dm::KM * cst + (size_t)by * a.Bxp + bx;
-        auto put = [&](int kk, double v) {
-            if (kk % DQ == gi) out[(size_t)kk * cst] = v;
-        };
-        put(Dm::C_N, nn);
-#pragma unroll
-        for (int j = 0; j < Q; ++j) put(Dm::C_U + j, fma(nn, (double)cs[j], (double)u[j]));
-        // S_ij = S'_ij + c_i u'_j + c_j u'_i + n c_i c_j
-#pragma unroll
-        for (int i = 0; i < Q; ++i)
-#pragma unroll
-            for (int j = i; j < Q; ++j) {
-                double v = (double)sv[Dm::s_idx(i, j) - Dm::C_S];
-                v = fma((double)cs[i], (double)u[j], v);
-                v = fma((double)cs[j], (double)u[i], v);
-                v = fma(nn * (double)cs[i], (double)cs[j], v);
-                put(Dm::s_idx(i, j), v);
-            }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) put(Dm::C_Y + c, (double)yc[c]);
-#pragma unroll
-        for (int j = 0; j < Q; ++j)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                put(Dm::C_XY + j * 3 + c, fma((double)cs[j], (double)yc[c], (double)xy[j * 3 + c]));
-        }
-    }
+    for (int it = blockIdx.x * NC + w; it < nitems; it += GW)
+        fit_consume_item<Q, D, MOD, HG>(a, it, per_frame, ring, full + w * S, empty + w * S, k, lane, waited);
     if (threadIdx.x == 0) FLR_TL(0, 2);
 }
 

@@ -9,6 +9,9 @@
 #include "flr_k2.cuh"
 #include "flr_fitws.cuh"
 #include "flr_applyws.cuh"
+#if FLR_Q == 4 || FLR_Q == 8
+#include "flr_wave.cuh"
+#endif
 #include <algorithm>
 #include <cstring>
 
@@ -27,6 +30,11 @@ void launch_apply(int, int, int, int, int, int, const float*, int, const float*,
                   const float*, const float*, bool)
 {
     ctx.unsupported = true;
+}
+template <int Q>
+bool launch_wave(const WaveLaunch&, LaunchCtx&)
+{
+    return false;
 }
 #else
 template <class K>
@@ -74,26 +82,28 @@ static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
     a.early = early;
     const int items = n * By * a.nseg;
     if (hg) {  // fp16 guide planes: the warp-specialised kernel with a half-width guide stage
-        if (!make_tmap_planes_f16(&a.tg, G, W, H, n * Q, kFS, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3))
-            return;
         using C = FitWsCfg<Q, false, true>;
+        if (!make_tmap_planes_f16(&a.tg, G, W, H, n * Q, kFS, Q, C::RB) ||
+            !make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3, C::RB))
+            return;
         set_smem(k_fit_ws<Q, D, false, true>, C::SMEM);
         launch_pdl(k_fit_ws<Q, D, false, true>, dim3(min(num_sms(), cdiv(items, C::NC))), dim3(C::THREADS), C::SMEM, s,
                    a, n);
         return;
     }
     if (A) {  // modulated fit: the warp-specialised kernel with the albedo planes in its ring
-        if (!make_tmap_planes(&a.tg, G, W, H, n * Q, kFS, Q) || !make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3) ||
-            !make_tmap_planes(&a.ta, A, W, H, n * 3, kFS, 3))
-            return;
         using C = FitWsCfg<Q, true>;
+        if (!make_tmap_planes(&a.tg, G, W, H, n * Q, kFS, Q, C::RB) ||
+            !make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3, C::RB) || !make_tmap_planes(&a.ta, A, W, H, n * 3, kFS, 3, C::RB))
+            return;
         set_smem(k_fit_ws<Q, D, true>, C::SMEM);
         launch_pdl(k_fit_ws<Q, D, true>, dim3(min(num_sms(), cdiv(items, C::NC))), dim3(C::THREADS), C::SMEM, s, a, n);
         return;
     }
-    if (vec_ok(G, W) && vec_ok(Y, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, kFS, Q) &&
-        make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3)) {  // default: one producer warp feeds 7 consumer warps
-        using C = FitWsCfg<Q>;
+    using CF = FitWsCfg<Q>;
+    if (vec_ok(G, W) && vec_ok(Y, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, kFS, Q, CF::RB) &&
+        make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3, CF::RB)) {  // default: one producer warp feeds 7 consumers
+        using C = CF;
         set_smem(k_fit_ws<Q, D>, C::SMEM);
         launch_pdl(k_fit_ws<Q, D>, dim3(min(num_sms(), cdiv(items, C::NC))), dim3(C::THREADS), C::SMEM, s, a, n);
         return;
@@ -201,7 +211,7 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
     if (hg) {  // fp16 guide planes (caller checked half_guides_apply_ok)
         ApplyArgs a;
         std::memset(&a, 0, sizeof(a));
-        if (mstride != Dims<Q>::MSTRIDE || !make_tmap_planes_f16(&a.tg, G, W, H, n * Q, kSeg, Q)) {
+        if (mstride != Dims<Q>::MSTRIDE || !make_tmap_planes_f16(&a.tg, G, W, H, n * Q, kSeg, Q, ApplyWsCfg<Q, false, true>::RB)) {
             ctx.unsupported = true;
             return;
         }
@@ -227,9 +237,10 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
     } else if (A) {  // modulated apply (caller checked apply_mod_fused): warp-specialised kernel only
         ApplyArgs a;
         std::memset(&a, 0, sizeof(a));
-        if (mstride != Dims<Q>::MSTRIDE || !make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q) ||
-            !make_tmap_planes(&a.ta, A, W, H, n * 3, kSeg, 3) ||
-            (Dl && !make_tmap_planes(&a.td, Dl, W, H, n * 3, kSeg, 3))) {
+        constexpr int RB = ApplyWsCfg<Q, true>::RB;
+        if (mstride != Dims<Q>::MSTRIDE || !make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q, RB) ||
+            !make_tmap_planes(&a.ta, A, W, H, n * 3, kSeg, 3, RB) ||
+            (Dl && !make_tmap_planes(&a.td, Dl, W, H, n * 3, kSeg, 3, RB))) {
             ctx.unsupported = true;
             return;
         }
@@ -251,21 +262,25 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
     if (D % 8 == 0 && mstride == Dims<Q>::MSTRIDE && aligned(models, 16)) {
         const int off = (D / 2) % 8;
         ApplyArgs a;
-        if (vec_ok(G, W) && vec_ok(out, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q)) {  // TMA path
+        int nsub = 1;  // sub-bands of >= 4 rows
+        while (D % (2 * nsub) == 0 && D / (2 * nsub) >= 4)
+            nsub *= 2;
+        const int items0 = n * cdiv(W, kSeg) * apply_nband(H, D, By) * nsub;
+        const bool ring = items0 >= 4 * num_sms() * ApplyCfg<Q>::NSW;  // batches: per-warp self-feeding rings
+        if (vec_ok(G, W) && vec_ok(out, W) &&
+            make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q, ring ? 1 : ApplyWsCfg<Q>::RB)) {  // TMA path
             a.models = models, a.out = out;
             a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W, kSeg), a.nband = apply_nband(H, D, By);
             using C = ApplyCfg<Q>;
             // sub-bands of >= 4 rows: finer items balance the warps (a single 1080p frame
             // otherwise leaves most warps with 1 item and some with 2; measured 28 -> 25 us)
-            a.nsub = 1;
-            while (D % (2 * a.nsub) == 0 && D / (2 * a.nsub) >= 4)
-                a.nsub *= 2;
+            a.nsub = nsub;
             a.reverse = 1;  // bottom-up: the fit's last rows are the likeliest still in L2
             const int items = n * a.nseg * a.nband * a.nsub;
             // many items (batches): the 11-warp self-feeding rings keep more rows in flight;
             // few items (one frame): the warp-specialised kernel's faster items win
             // (measured 1080p: 1 frame 22.6 vs 26.6 us, 8 frames 17.8 vs 16.2 us per frame)
-            if (items >= 4 * num_sms() * ApplyCfg<Q>::NSW) {  // per-warp self-feeding rings
+            if (ring) {  // per-warp self-feeding rings (one row per box)
                 using C = ApplyCfg<Q>;
                 const int grid = min(num_sms(), cdiv(items, C::NSW));
                 ctx.before("k_apply_stream");
@@ -293,6 +308,65 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
         k_apply_px<Q><<<grid, block, 0, s>>>(W, H, D, Bx, By, models, mstride, G, out);
     }
 }
+template <int Q>
+bool launch_wave(const WaveLaunch& L, LaunchCtx& ctx)
+{
+#if FLR_Q == 4 || FLR_Q == 8
+    const int Dout = L.D * L.U, R = L.taps.R;
+    const int Wo = L.W * L.U, Ho = L.H * L.U;
+    if (!(L.D == 4 || L.D == 8) || Dout % 8 || !(R == 3 || R == 5)) return false;
+    if (!vec_ok(L.G, L.W) || !vec_ok(L.Y, L.W) || !vec_ok(L.Gout, Wo) || !vec_ok(L.out, Wo) || !aligned(L.models, 16))
+        return false;
+    if ((size_t)L.n * L.By * cdiv(L.W, kFS) >= (1u << 30)) return false;
+    WaveArgs w;
+    std::memset(&w, 0, sizeof(w));
+    const int Bxp = mom_pitch(L.Bx);
+    if (!make_tmap_planes(&w.fit.tg, L.G, L.W, L.H, L.n * Q, kFS, Q, 2) ||
+        !make_tmap_planes(&w.fit.ty, L.Y, L.W, L.H, L.n * 3, kFS, 3, 2) ||
+        !make_tmap_planes(&w.app.tg, L.Gout, Wo, Ho, L.n * Q, kSeg, Q, 2))
+        return false;
+    auto tmom = [&](auto KGv) {
+        using KG = decltype(KGv);
+        return make_tmap_3d(&w.tmom, L.mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, L.Bx, L.By, Bxp, L.n * Dims<Q>::KM, KG::HX,
+                            KG::NV, KG::G);
+    };
+    if (!(R == 3 ? tmom(K2Geom<Q, 3>{}) : tmom(K2Geom<Q, 5>{}))) return false;
+    w.fit.mom = L.mom;
+    w.fit.W = L.W, w.fit.H = L.H, w.fit.Bx = L.Bx, w.fit.Bxp = Bxp, w.fit.By = L.By, w.fit.nseg = cdiv(L.W, kFS);
+    w.app.models = L.models, w.app.out = L.out;
+    w.app.W = Wo, w.app.H = Ho, w.app.D = Dout, w.app.Bx = L.Bx, w.app.By = L.By;
+    w.app.nseg = cdiv(Wo, kSeg), w.app.nband = apply_nband(Ho, Dout, L.By);
+    w.app.nsub = 1;
+    while (Dout % (2 * w.app.nsub) == 0 && Dout / (2 * w.app.nsub) >= 4)
+        w.app.nsub *= 2;
+    w.taps = L.taps;
+    w.eps_add = L.eps_add, w.eps_mul = L.eps_mul;
+    w.n = L.n;
+    w.nfit = L.n * L.By * w.fit.nseg, w.nfc = cdiv(w.nfit, kWaveNC);
+    w.napp = L.n * w.app.nband * w.app.nsub * w.app.nseg;
+    w.ntr = cdiv(L.By, kK2TY), w.ntc = cdiv(L.Bx, kK2TX);
+    w.flags = L.flags;
+    // the queue heads and row counters start at zero.  The kernel is launched WITHOUT
+    // programmatic dependent launch: a PDL launch may overlap the preceding kernel across
+    // this memset (in a graph the memset then races the running kernel)
+    cudaMemsetAsync(L.flags, 0, sizeof(int) * (size_t)wave_flags_ints(L.n, L.By), ctx.s);
+#define FLR_WAVE_L(DD, RR)                                                                        \
+    if (L.D == DD && R == RR) {                                                                   \
+        using C = WaveCfg<Q, RR>;                                                                 \
+        set_smem(k_flr_wave<Q, DD, RR>, C::SMEM);                                                 \
+        ctx.before("k_flr_wave");                                                                 \
+        k_flr_wave<Q, DD, RR><<<dim3(num_sms()), dim3(C::THREADS), C::SMEM, ctx.s>>>(w);           \
+        return true;                                                                              \
+    }
+    FLR_WAVE_L(4, 3) FLR_WAVE_L(4, 5) FLR_WAVE_L(8, 3) FLR_WAVE_L(8, 5)
+#undef FLR_WAVE_L
+    return false;
+#else
+    (void)L;
+    (void)ctx;
+    return false;
+#endif
+}
 
 #endif  // FLR_STUB
 
@@ -311,5 +385,6 @@ bool apply_mod_supported()
 #endif
 }
 template bool apply_mod_supported<FLR_Q>();
+template bool launch_wave<FLR_Q>(const WaveLaunch&, LaunchCtx&);
 
 }  // namespace flr

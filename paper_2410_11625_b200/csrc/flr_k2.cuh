@@ -56,42 +56,34 @@ struct K2Geom {
     static_assert(SMEM <= 232448, "K2 tile exceeds 227 KB of shared memory");
 };
 
-// tm: the fp64 moment field [n*KM][By][Bxp] with box {HX, TY + 2R, G} (K2Geom)
+// One TX x TY tile of output blocks (frame f, first block (bx0, by0)), run by the kK2Threads
+// threads of the CTA (tid = threadIdx.x).  smk: KG::BAR_OFF bytes of shared memory, bar: S
+// mbarriers, initialised here (every earlier use of them must have completed).
+// tm: the fp64 moment field [n*KM][By][Bxp] with box {HX, TY + 2R, G} (K2Geom).
 template <int Q, int R>
-__global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
-    k_blur_solve_tile(const __grid_constant__ CUtensorMap tm, int Bx, int By, float* __restrict__ models,
-                      int mstride, double eps_add, double eps_mul, const __grid_constant__ Taps t)
+__device__ __forceinline__ void k2_tile(const CUtensorMap* tmp, int f, int bx0, int by0, int Bx, int By,
+                                        float* __restrict__ models, int mstride, double eps_add, double eps_mul,
+                                        const Taps& t, double* smk, uint64_t* bar, uint64_t kpol)
 {
     using Dm = Dims<Q>;
     using KG = K2Geom<Q, R>;
     constexpr int KM = Dm::KM, G = KG::G, NG = KG::NG, HX = KG::HX, NV = KG::NV, RE = KG::RE, S = KG::S, VT = KG::VT;
     constexpr int TX = kK2TX, TY = kK2TY, VP = KG::VP, SP = KG::SP, NCH = KG::NCH, MS = Dm::MSTRIDE;
-    extern __shared__ __align__(1024) double smk[];
     double* ring = smk;
     double* vb = smk + S * KG::BOX;
     double* st = vb + KG::VB;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(smk) + KG::BAR_OFF);
     const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-    if (tid == 0) FLR_TL(1, 0);
-    const int bx0 = blockIdx.x * TX, by0 = blockIdx.y * TY, f = blockIdx.z;
-#ifdef FLR_DBG_PHASES
-    extern __device__ long long g_flr_phase[];
-    const int cta_id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    if (tid == 0) g_flr_phase[1000 + 4 * cta_id] = gtimer();
-#endif
+    const CUtensorMap& tm = *tmp;
     auto issue = [&](int grp) {
         uint64_t* b = &bar[grp % S];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage before
         mbar_arrive_expect_tx(b, KG::BOXD * sizeof(double));
-        tma_load_3d(ring + (grp % S) * KG::BOX, &tm, bx0 - RE, by0 - R, f * KM + grp * G, b, policy_evict_normal());
+        tma_load_3d(ring + (grp % S) * KG::BOX, &tm, bx0 - RE, by0 - R, f * KM + grp * G, b, kpol);
     };
     if (tid == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
     }
-    pdl_wait();  // the moment field comes from the previous grid
-    pdl_trigger();  // dependents launch only once we are past our own wait
-    if (tid == 0) FLR_TL(1, 1);
     __syncthreads();
     if (tid == 0)
         for (int g = 0; g < S && g < NG; ++g) issue(g);
@@ -106,27 +98,21 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
         tsg[grp + 1] = clock64();
 #endif
         mbar_wait(&bar[grp % S], (grp / S) & 1);
-        {
+        {  // v-pass, one column task at a time (keeps the live set to NV values besides blur[])
             const double* box = ring + (grp % S) * KG::BOX;
-            double v[VT][NV];
 #pragma unroll
             for (int q = 0; q < VT; ++q) {
                 const int task = tid + q * kK2Threads, gv = task / HX, u = task - gv * HX;
                 if (gv < G) {
+                    double v[NV];
 #pragma unroll
-                    for (int i = 0; i < NV; ++i) v[q][i] = box[(gv * NV + i) * HX + u];
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < VT; ++q) {
-                const int task = tid + q * kK2Threads, gv = task / HX, u = task - gv * HX;
-                if (gv < G) {
+                    for (int i = 0; i < NV; ++i) v[i] = box[(gv * NV + i) * HX + u];
                     double* o = vb + gv * TY * VP + u + 2 * (u / 8);
 #pragma unroll
                     for (int r = 0; r < TY; ++r) {
-                        double a = t.g[R] * v[q][r + R];
+                        double a = t.g[R] * v[r + R];
 #pragma unroll
-                        for (int d = 1; d <= R; ++d) a = fma(t.g[R + d], v[q][r + R - d] + v[q][r + R + d], a);
+                        for (int d = 1; d <= R; ++d) a = fma(t.g[R + d], v[r + R - d] + v[r + R + d], a);
                         o[r * VP] = a;
                     }
                 }
@@ -201,7 +187,23 @@ __global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
             models[((size_t)(f * By + by0 + r) * Bx + bx0) * mstride + j] = mstage[(r * TX + b) * MS + j - b * mstride];
         }
     }
-    if (tid == 0) FLR_TL(1, 2);
+}
+
+template <int Q, int R>
+__global__ void __launch_bounds__(kK2Threads, kK2MinBlocks)
+    k_blur_solve_tile(const __grid_constant__ CUtensorMap tm, int Bx, int By, float* __restrict__ models,
+                      int mstride, double eps_add, double eps_mul, const __grid_constant__ Taps t)
+{
+    using KG = K2Geom<Q, R>;
+    extern __shared__ __align__(1024) double smk[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(smk) + KG::BAR_OFF);
+    if (threadIdx.x == 0) FLR_TL(1, 0);
+    pdl_wait();  // the moment field comes from the previous grid
+    pdl_trigger();  // dependents launch only once we are past our own wait
+    if (threadIdx.x == 0) FLR_TL(1, 1);
+    k2_tile<Q, R>(&tm, blockIdx.z, blockIdx.x * kK2TX, blockIdx.y * kK2TY, Bx, By, models, mstride, eps_add, eps_mul, t,
+                  smk, bar, policy_evict_normal());
+    if (threadIdx.x == 0) FLR_TL(1, 2);
 }
 
 }  // namespace flr

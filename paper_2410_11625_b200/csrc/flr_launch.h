@@ -38,10 +38,10 @@ inline bool make_tmap_3d(CUtensorMap* m, const void* base, CUtensorMapDataType d
                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// fp32 planes [planes][H][W], box {bx, 1, bz}
-inline bool make_tmap_planes(CUtensorMap* m, const float* base, int W, int H, int planes, int bx, int bz)
+// fp32 planes [planes][H][W], box {bx, by, bz}
+inline bool make_tmap_planes(CUtensorMap* m, const float* base, int W, int H, int planes, int bx, int bz, int by = 1)
 {
-    return make_tmap_3d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, W, planes, bx, 1, bz);
+    return make_tmap_3d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, W, H, W, planes, bx, by, bz);
 }
 // moment-field row pitch (elements): even, so rows are 16-byte aligned for TMA
 inline int mom_pitch(int Bx) { return (Bx + 1) & ~1; }
@@ -103,10 +103,11 @@ inline bool half_guides_apply_ok(int D, int W, const void* models, const void* G
 {
     return D % 8 == 0 && aligned(models, 16) && aligned(G, 16) && W % 8 == 0 && vec_ok(out, W);
 }
-// fp16 planes [planes][H][W], box {bx, 1, bz}
-inline bool make_tmap_planes_f16(CUtensorMap* m, const void* base, int W, int H, int planes, int bx, int bz)
+// fp16 planes [planes][H][W], box {bx, by, bz}
+inline bool make_tmap_planes_f16(CUtensorMap* m, const void* base, int W, int H, int planes, int bx, int bz,
+                                 int by = 1)
 {
-    return make_tmap_3d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W, H, W, planes, bx, 1, bz);
+    return make_tmap_3d(m, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W, H, W, planes, bx, by, bz);
 }
 
 // shapes for which the modulated (albedo) protocol runs fused into the TMA kernels
@@ -123,6 +124,28 @@ inline bool apply_mod_fused(int D, int W, const void* models, const void* G, con
            (!Dl || vec_ok(Dl, W));
 }
 
+// the one-kernel wavefront schedule (flr_wave.cuh).  Returns false, launching nothing,
+// when the shape is not compiled in (Q in {4, 8}, block in {4, 8}, R in {3, 5}, output
+// block a multiple of 8, 16-byte aligned planes with W % 4 == 0): the caller then runs
+// the staged kernels.
+struct WaveLaunch {
+    int n, W, H, D, U, Bx, By;    // fit resolution, block size, upsample
+    const float *G, *Y, *Gout;    // fit guides, fit radiance, output-resolution guides
+    float* out;
+    double* mom;                  // [n][KM][By][Bxp]
+    float* models;                // padded [n][By][Bx][MSTRIDE]
+    int* flags;                   // wave_flags_ints(n, By) ints of workspace
+    double eps_add, eps_mul;
+    Taps taps;
+};
+#ifdef FLR_WAVE_TRACE
+inline int wave_flags_ints(int n, int By) { return 4 + n * (By + 3 * ((By + 7) / 8) + 2) + 4 * 96 * 160 + 2; }
+#else
+inline int wave_flags_ints(int n, int By) { return 4 + n * (By + 3 * ((By + 7) / 8) + 2); }
+#endif
+template <int Q>
+bool launch_wave(const WaveLaunch& L, LaunchCtx& ctx);
+
 #define FLR_DECLARE_Q(Q)                                                                          \
     extern template void launch_fit<Q>(int, int, int, int, int, int, const float*, const float*,  \
                                        float*, double*, double*, float*, int, double, double,     \
@@ -130,7 +153,8 @@ inline bool apply_mod_fused(int D, int W, const void* models, const void* G, con
     extern template void launch_apply<Q>(int, int, int, int, int, int, const float*, int,         \
                                          const float*, float*, LaunchCtx&, const float*,          \
                                          const float*, bool);                                     \
-    extern template bool apply_mod_supported<Q>();
+    extern template bool apply_mod_supported<Q>();                                              \
+    extern template bool launch_wave<Q>(const WaveLaunch&, LaunchCtx&);
 FLR_DECLARE_Q(1) FLR_DECLARE_Q(2) FLR_DECLARE_Q(3) FLR_DECLARE_Q(4) FLR_DECLARE_Q(5)
 FLR_DECLARE_Q(6) FLR_DECLARE_Q(7) FLR_DECLARE_Q(8) FLR_DECLARE_Q(9) FLR_DECLARE_Q(10)
 FLR_DECLARE_Q(11) FLR_DECLARE_Q(12) FLR_DECLARE_Q(13) FLR_DECLARE_Q(14) FLR_DECLARE_Q(15)

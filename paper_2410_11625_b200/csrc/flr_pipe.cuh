@@ -4,6 +4,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#ifdef FLR_WATCHDOG
+#include <cstdio>
+#endif
 
 namespace flr {
 
@@ -50,11 +53,27 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, unsigned parity)  
         : "memory");
     return ok != 0;
 }
+#ifdef FLR_WATCHDOG
+// debug builds: a wait that has not completed after ~2^32 cycles reports itself and traps
+__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, unsigned parity, int line)
+{
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity)) {
+        if (clock64() - t0 > (1ll << 32)) {
+            printf("FLR watchdog: mbar_wait line %d block %d thread %d bar_off %u parity %u\n", line, blockIdx.x,
+                   threadIdx.x, (unsigned)__cvta_generic_to_shared(bar), parity);
+            __trap();
+        }
+    }
+}
+#define mbar_wait(b, p) mbar_wait_dbg((b), (p), __LINE__)
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity)
 {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+#endif
 
 // Producer side of a warp-specialised ring, before a TMA write into a stage the consumers
 // have read: a generic -> async proxy fence (conservative; measured free, FLR_WS_NO_PROXY_FENCE
@@ -160,6 +179,22 @@ __device__ __forceinline__ int ld_relaxed(const int* p)
     return v;
 }
 __device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v)
+{
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ int atom_cas_acq_rel(int* p, int cmp, int v)
+{
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_release_max(int* p, int v)
+{
+    asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_add(int* p, int v)
 {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

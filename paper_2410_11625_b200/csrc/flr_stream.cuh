@@ -111,17 +111,19 @@ struct FitArgs {
 };
 
 // HG: the guide planes are IEEE binary16 (half the stage bytes of the guides)
-// SW: segment width in pixels (the TMA box width of every plane)
-template <int Q, int D, bool MOD = false, bool HG = false, int SW = kSeg>
+// SW: segment width in pixels (the TMA box width of every plane); RB: pixel rows per box
+// (the tensor maps' box height).  Stage layout: [Q planes][RB rows][SW] guides, then
+// [3 (+3) planes][RB rows][SW] radiance (+ albedo); rows past the image arrive as zeros.
+template <int Q, int D, bool MOD = false, bool HG = false, int SW = kSeg, int RB = 1>
 __device__ __forceinline__ void fit_issue_row(const FitArgs& a, int f, int by, int sg, int rr, float* dst,
                                               uint64_t* bar, uint64_t pol_g, uint64_t pol_y)
 {
-    constexpr int GF = HG ? SW / 2 : SW;  // floats of stage per guide plane
-    mbar_arrive_expect_tx(bar, (Q * GF + (3 + (MOD ? 3 : 0)) * SW) * 4);
+    constexpr int GF = HG ? SW / 2 : SW;  // floats of stage per guide plane row
+    mbar_arrive_expect_tx(bar, RB * (Q * GF + (3 + (MOD ? 3 : 0)) * SW) * 4);
     const int x = sg * SW, y = by * D + rr;
     tma_load_3d(dst, &a.tg, x, y, f * Q, bar, pol_g);
-    tma_load_3d(dst + Q * GF, &a.ty, x, y, f * 3, bar, pol_y);
-    if (MOD) tma_load_3d(dst + Q * GF + 3 * SW, &a.ta, x, y, f * 3, bar, pol_y);
+    tma_load_3d(dst + RB * Q * GF, &a.ty, x, y, f * 3, bar, pol_y);
+    if (MOD) tma_load_3d(dst + RB * (Q * GF + 3 * SW), &a.ta, x, y, f * 3, bar, pol_y);
 }
 
 // ============================================================================
@@ -185,17 +187,19 @@ __device__ __forceinline__ void apply_issue_models(const ApplyArgs& a, const App
     bulk_g2s(dst + kApplyNCol * SD::MS, M + ((size_t)g.j1 * a.Bx + g.ic0) * SD::MS, mb, bar, pol_m);
 }
 
-// guide row y of an APPLY item (lane 0)
-template <int Q, bool MOD = false, bool HG = false>
+// guide rows y .. y + RB - 1 of an APPLY item (one box per tensor; the tensor maps' box
+// height is RB).  Stage layout: [Q][RB][128] guides, then [3][RB][128] albedo and
+// [3][RB][128] direct light (modulated apply only)
+template <int Q, bool MOD = false, bool HG = false, int RB = 1>
 __device__ __forceinline__ void apply_issue_row(const ApplyArgs& a, const ApplyGeom& g, int f, int y, float* dst,
                                                 uint64_t* bar, uint64_t pol_g)
 {
-    constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats of stage per guide plane
-    mbar_arrive_expect_tx(bar, (Q * GF + (MOD ? (a.has_direct ? 6 : 3) : 0) * kSeg) * 4);
+    constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats of stage per guide plane row
+    mbar_arrive_expect_tx(bar, RB * (Q * GF + (MOD ? (a.has_direct ? 6 : 3) : 0) * kSeg) * 4);
     tma_load_3d(dst, &a.tg, g.xs, y, f * Q, bar, pol_g);
     if (MOD) {  // remodulation planes: albedo, then the direct light
-        tma_load_3d(dst + Q * GF, &a.ta, g.xs, y, f * 3, bar, pol_g);
-        if (a.has_direct) tma_load_3d(dst + Q * GF + 3 * kSeg, &a.td, g.xs, y, f * 3, bar, pol_g);
+        tma_load_3d(dst + RB * Q * GF, &a.ta, g.xs, y, f * 3, bar, pol_g);
+        if (a.has_direct) tma_load_3d(dst + RB * (Q * GF + 3 * kSeg), &a.td, g.xs, y, f * 3, bar, pol_g);
     }
 }
 

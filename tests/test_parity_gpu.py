@@ -173,12 +173,12 @@ def test_stress_fireflies_and_crowded_depth(flr, oracle_mod):
 
 
 # ------------------------------------------------------------------ schedules
-@pytest.mark.parametrize("variant", [1])
+@pytest.mark.parametrize("variant", [1, 2])
 @pytest.mark.parametrize("W,H,Q,block,sigma,n", [(1920, 1080, 8, 8, 10.0, 1), (640, 360, 8, 8, 20.0, 2),
                                                  (512, 256, 4, 8, 10.0, 3), (264, 136, 8, 8, 12.0, 1)])
 def test_variants_match_oracle(flr, oracle_mod, variant, W, H, Q, block, sigma, n):
-    """Both kernel schedules (STAGED = 3 launches, FUSED = one persistent wavefront kernel)
-    meet the parity bar; multi-frame calls exercise the fused schedule's frame sequencing."""
+    """Both kernel schedules (STAGED = 3 launches, FUSED = one persistent wavefront kernel,
+    k_flr_wave) meet the parity bar; multi-frame calls exercise the wave's frame sequencing."""
     from paper_2410_11625_b200 import synth
 
     G, Y = synth.batch(n, W, H, Q=Q, seed0=4000 + W + variant)
@@ -186,7 +186,9 @@ def test_variants_match_oracle(flr, oracle_mod, variant, W, H, Q, block, sigma, 
     torch.cuda.synchronize()
     names = flr.last_launch_names()
     if variant == 2:
-        assert names == ["k_flr_fused"], names
+        assert names == ["k_flr_wave"], names
+        ref_staged = flr.denoise(G.cuda(), Y.cuda(), block=block, sigma=sigma, variant=1)
+        assert torch.equal(out, ref_staged), "wave schedule differs from the staged kernels"
     R = flr.effective_radius(block=block, sigma=sigma)
     ref = oracle_mod.denoise(G.numpy(), Y.numpy(), D=block, sigma=sigma, R=R)
     assert_parity(out.cpu().numpy(), ref, f"variant {variant} {W}x{H} Q={Q} n={n}")
@@ -235,3 +237,47 @@ def test_errors_raise(flr):
 def test_parity_report_helper():
     r = parity_report(np.array([1.0, 2.0]), np.array([1.0, 2.0001]))
     assert r["violations"] == 0
+
+
+# ------------------------------------------------------------------ wave schedule (FUSED)
+def test_wave_upsample(flr, oracle_mod):
+    """C4's shape through the one-kernel wave schedule (fit at D=4, apply at D_out=8)."""
+    from paper_2410_11625_b200 import synth
+
+    g_lo, y_lo, g_hi = synth.upsample_pair(480, 272, U=2, Q=8, seed=4100)
+    out = flr.denoise_upsample(g_lo.cuda(), y_lo.cuda(), g_hi.cuda(), block=4, upsample=2, variant=2)
+    torch.cuda.synchronize()
+    assert flr.last_launch_names() == ["k_flr_wave"]
+    staged = flr.denoise_upsample(g_lo.cuda(), y_lo.cuda(), g_hi.cuda(), block=4, upsample=2, variant=1)
+    assert torch.equal(out, staged)
+    ref = oracle_mod.denoise_upsample(g_lo.numpy(), y_lo.numpy(), g_hi.numpy(), D_fit=4, U=2, sigma=10.0, R=3)
+    assert_parity(out.cpu().numpy(), ref, "wave upsample")
+
+
+def test_wave_back_to_back(flr):
+    """Many wave calls issued back to back on one stream and one workspace (the queue heads
+    and row counters are reset per call), with staged calls interleaved: every result equals
+    the staged kernels' bit for bit, and nothing hangs."""
+    from paper_2410_11625_b200 import synth
+
+    W, H = 1920, 1080
+    frames = [synth.batch(1, W, H, Q=8, seed0=5100 + k) for k in range(2)]
+    dev = [(g.cuda(), y.cuda()) for g, y in frames]
+    ref = [flr.denoise(g, y, variant=1) for g, y in dev]
+    ws = torch.zeros(flr.workspace_size(1, 8, W, H), dtype=torch.uint8, device="cuda")
+    outs = [torch.empty_like(ref[0]) for _ in range(16)]
+    for i in range(16):
+        g, y = dev[i % 2]
+        flr.denoise(g, y, variant=2 if i % 4 else 1, workspace=ws, out=outs[i])
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        assert torch.equal(o, ref[i % 2]), f"call {i}"
+
+
+def test_wave_unsupported_shape(flr):
+    """FUSED outside the compiled shapes reports FLR_ERR_UNSUPPORTED (Q=5 is not compiled)."""
+    from paper_2410_11625_b200 import synth
+
+    G, Y = synth.batch(1, 128, 64, Q=5, seed0=5200)
+    with pytest.raises(flr.FLRError):
+        flr.denoise(G.cuda(), Y.cuda(), variant=2)

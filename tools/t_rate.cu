@@ -1,0 +1,67 @@
+// Per-SM streaming rate of the warp-specialised fit and apply kernels: 8 distinct 1080p Q=8
+// frames (730 MB of inputs, > L2) processed with the grid restricted to G CTAs (one per SM),
+// G = 148 ... 37.  If the kernels are HBM-bound, time stays flat as G shrinks until the
+// per-SM rate limit is reached; the knee gives the rate one SM can stream at.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude -lcuda tools/t_rate.cu -o tools/t_rate
+#include <cstdio>
+#include "../paper_2410_11625_b200/csrc/flr_launch.h"
+#include "../paper_2410_11625_b200/csrc/flr_fitws.cuh"
+#include "../paper_2410_11625_b200/csrc/flr_applyws.cuh"
+using namespace flr;
+int main()
+{
+    constexpr int Q = 8, D = 8;
+    const int W = 1920, H = 1080, NF = 8, Bx = W / D, By = (H + D - 1) / D;
+    const size_t plane = (size_t)W * H;
+    float *G, *Y, *M, *O;
+    double* mom;
+    cudaMalloc(&G, plane * Q * NF * 4);
+    cudaMalloc(&Y, plane * 3 * NF * 4);
+    cudaMalloc(&O, plane * 3 * NF * 4);
+    cudaMalloc(&M, (size_t)Bx * By * NF * Dims<Q>::MSTRIDE * 4);
+    cudaMalloc(&mom, (size_t)mom_pitch(Bx) * By * NF * Dims<Q>::KM * 8);
+    cudaMemset(G, 0, plane * Q * NF * 4);
+    cudaMemset(Y, 0, plane * 3 * NF * 4);
+    cudaMemset(M, 0, (size_t)Bx * By * NF * Dims<Q>::MSTRIDE * 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    using FC = FitWsCfg<Q>;
+    using AC = ApplyWsCfg<Q>;
+    cudaFuncSetAttribute(k_fit_ws<Q, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM);
+    cudaFuncSetAttribute(k_apply_ws<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AC::SMEM);
+    const int nf = NF;
+    FitArgs fa{};
+    make_tmap_planes(&fa.tg, G, W, H, nf * Q, kFS, Q, FitWsCfg<Q>::RB);
+    make_tmap_planes(&fa.ty, Y, W, H, nf * 3, kFS, 3, FitWsCfg<Q>::RB);
+    fa.mom = mom, fa.W = W, fa.H = H, fa.Bx = Bx, fa.Bxp = mom_pitch(Bx), fa.By = By, fa.nseg = W / kFS;
+    ApplyArgs aa{};
+    make_tmap_planes(&aa.tg, G, W, H, nf * Q, kSeg, Q, ApplyWsCfg<Q>::RB);
+    aa.models = M, aa.out = O, aa.W = W, aa.H = H, aa.D = D, aa.Bx = Bx, aa.By = By;
+    aa.nseg = W / kSeg, aa.nband = apply_nband(H, D, By), aa.nsub = 2;
+    const double fit_bytes = (double)plane * (Q + 3) * 4 * nf, app_bytes = (double)plane * (Q + 3) * 4 * nf;
+    for (int g : {148, 136, 120, 104, 88, 74, 60, 48, 37}) {
+        float ms = 0;
+        const int reps = 30;
+        for (int k = 0; k < 2; ++k) {
+            cudaEventRecord(e0);
+            for (int r = 0; r < reps; ++r) k_fit_ws<Q, D><<<g, FC::THREADS, FC::SMEM>>>(fa, nf);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+        }
+        const double tf = 1e-3 * ms / reps;
+        for (int k = 0; k < 2; ++k) {
+            cudaEventRecord(e0);
+            for (int r = 0; r < reps; ++r) k_apply_ws<Q><<<g, AC::THREADS, AC::SMEM>>>(aa, nf);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+        }
+        const double ta = 1e-3 * ms / reps;
+        printf("G=%3d  fit %7.2f us/frame %6.0f GB/s (%5.1f GB/s/SM)   apply %7.2f us/frame %6.0f GB/s (%5.1f GB/s/SM)  %s\n",
+               g, 1e6 * tf / nf, fit_bytes / tf / 1e9, fit_bytes / tf / 1e9 / g, 1e6 * ta / nf, app_bytes / ta / 1e9,
+               app_bytes / ta / 1e9 / g, cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
