@@ -121,11 +121,11 @@ def _apply_mod_bytes(c):  # + 3 albedo and 3 direct-light planes
 KERNEL_BYTES = {
     "k_fit_ws_mod": _fit_mod_bytes, "k_apply_ws_mod": _apply_mod_bytes,
     # algorithmic bytes per frame of each launch: the full-resolution planes it must read + write
-    "k_fit_moments": _fit_bytes, "k_fit_stream": _fit_bytes, "k_fit_ldg": _fit_bytes, "k_fit_ws": _fit_bytes,
+    "k_fit_moments": _fit_bytes, "k_fit_ws": _fit_bytes, "k_fit_ws_f64acc": _fit_bytes,
     "k_fit_ws_f16": _fit_bytes,
-    "k_apply_stream": _apply_bytes, "k_apply_tile": _apply_bytes, "k_apply_px": _apply_bytes,
+    "k_apply_tile": _apply_bytes, "k_apply_px": _apply_bytes, "k_apply_centered": _apply_bytes,
     "k_apply_ws": _apply_bytes, "k_apply_ws_f16": _apply_bytes,
-    "k_flr_fused": lambda c: min_bytes_per_frame(c),
+    "k_flr_wave": lambda c: min_bytes_per_frame(c),
 }
 
 
@@ -145,7 +145,6 @@ def k2_flops_per_frame(c):
 
 KERNEL_FLOPS = {  # fp64-bound kernels
     "k_blur_solve_tile": k2_flops_per_frame,
-    "k_blur_solve": k2_flops_per_frame,
 }
 # DP peak from the unit count: 148 SMs x 64 FP64 FMA/clk (measured 63/clk/SM with a DFMA
 # microbenchmark, tools/ubench_fma.cu) x 2 flops x 1.965 GHz
@@ -168,6 +167,22 @@ def ncu_traffic(kernel, config):
     try:
         d = json.load(open(p))
         return d.get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def step_traffic(config, variant, frames):
+    """Whole-step DRAM bytes of one call from the committed ncu app-range capture
+    (profiles/r02_step_traffic.json, tools/step_traffic.py), c2 single-frame steps only."""
+    p = os.path.join(ROOT, "profiles", "r02_step_traffic.json")
+    if config != "c2" or frames != 1 or not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))["fused" if variant == 2 else "staged"]
+        return {"dram_bytes": d["dram_bytes"], "dram_read_bytes": d["dram_read_bytes"],
+                "dram_write_bytes": d["dram_write_bytes"], "bytes_per_output_px": d["dram_bytes_per_output_px"],
+                "source": "profiles/r02_step_traffic.json (ncu app-range replay of one call; write-back of "
+                          "dirty L2 lines after the range is not counted)"}
     except Exception:
         return None
 
@@ -666,7 +681,8 @@ def run_flr(args, cfg, rank, world, local_rank):
     step_ms = ms_max / args.steps  # c5: one pass over the rank's shard of the batch
     step_bytes = min_bytes_per_frame(cfg) * (nsh if batch else F)
     step_roof = {"min_bytes_per_step": step_bytes, "achieved": step_bytes / (step_ms * 1e-3) / 1e9,
-                 "peak": peak, "unit": "GB/s", "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak}
+                 "peak": peak, "unit": "GB/s", "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak,
+                 "traffic": step_traffic(args.config, args.variant, F)}
     cpu_base = None
     if world == 1 and not args.no_cpu_baseline:
         cpu_base = oracle_sample(cfg, args.cpu_seconds, one_thread=True)

@@ -77,7 +77,8 @@ typedef enum {
                                their inputs complete (row wavefront; bitwise equal to STAGED).
                                Compiled for Q in {4, 8}, block in {4, 8}, radius in {3, 5},
                                output block a multiple of 8, 16-byte aligned planes with
-                               W % 4 == 0; FLR_ERR_UNSUPPORTED otherwise */
+                               W % 4 == 0, fp32 guides, the appendix solver;
+                               FLR_ERR_UNSUPPORTED otherwise */
 } flr_variant;
 
 /* Per-block solver. */
@@ -85,7 +86,11 @@ typedef enum {
     FLR_SOLVER_APPENDIX = 0, /* the paper's normalised, regularised solve, eps_add + eps_mul */
     FLR_SOLVER_TIKHONOV = 1  /* Eq. tikhonov with Fig. 3's semantics:
                                 A = (Mbar/n + eps_add I)^-1 Nbar/n on the full (Q+1) system, the
-                                bias included (R18, R22); eps_mul is ignored */
+                                bias included (R18, R22); eps_mul is ignored.  flr_fit returns
+                                raw-basis models; the denoise calls with fp32 guides evaluate
+                                each block's model about its window mean, b0 + A.(x - mu), and
+                                blend the four predictions (exact arithmetic: the same result;
+                                in fp32 it avoids cancelling slopes ~cov/eps against the bias) */
 } flr_solver;
 
 typedef struct {

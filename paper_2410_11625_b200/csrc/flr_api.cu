@@ -9,6 +9,8 @@
 #include "../../include/flr.h"
 #include "flr_common.cuh"
 #include "flr_launch.h"
+#include "flr_solve.cuh"
+#include "flr_staged.cuh"
 
 using namespace flr;
 
@@ -38,7 +40,9 @@ flr_status check_params(const flr_params* p)
 
 // eps_mul as the kernels take it: a negative value selects the Tikhonov solve
 // (solve_block_tikhonov in flr_solve.cuh); users cannot pass one (check_params)
-inline double solver_eps_mul(const flr_params* p) { return p->solver == FLR_SOLVER_TIKHONOV ? -1.0 : p->eps_mul; }
+inline double solver_eps_mul(const flr_params* p) { return p->solver == FLR_SOLVER_TIKHONOV ? kTikhonovRaw : p->eps_mul; }
+// floats per block of the centred Tikhonov models ([b0 | slopes | mu], k_apply_centered)
+inline int centered_stride(int Q) { return 4 * (Q + 1); }
 
 // R1: default radius ceil(2 sigma / D_out) blocks (Fig. 3's 41-tap kernel at std 10)
 int effective_radius(const flr_params* p)
@@ -66,7 +70,7 @@ Layout layout(int n, int Q, int Bx, int By)
     L.hb = off;
     off += align256(nbp * km_of(Q) * sizeof(double));
     L.models = off;
-    off += align256(nb * mstride_of(Q) * sizeof(float));
+    off += align256(nb * (mstride_of(Q) > centered_stride(Q) ? mstride_of(Q) : centered_stride(Q)) * sizeof(float));
     L.flags = off;  // task-queue heads + row counters of the wave schedule (zeroed per call)
     off += align256(sizeof(int) * (size_t)wave_flags_ints(n, By));
     L.total = off;
@@ -148,7 +152,7 @@ flr_status check_ws(int n, int Q, int W, int H, const flr_params* p, void* ws, s
 // fit into `models` with `mstride` floats per block; arguments already validated
 flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, const flr_params* p,
                   float* models, int mstride, void* ws, LaunchCtx& ctx, bool hg = false,
-                  bool inputs_from_call = false)
+                  bool inputs_from_call = false, double eps_mul_override = 0.0)
 {
     const int D = p->block;
     const int Bx = cdiv(W, D), By = cdiv(H, D);
@@ -161,7 +165,8 @@ flr_status do_fit(int n, int Q, int W, int H, const float* G, const float* Y, co
     ctx.early = (p->flags & FLR_FLAG_INPUTS_READY) && !inputs_from_call;
     FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, G, Y, (float*)(base + L.raw),
                                       (double*)(base + L.mom), (double*)(base + L.hb), models,
-                                      mstride, p->eps_add, solver_eps_mul(p), taps, ctx, nullptr, 0.f, hg)));
+                                      mstride, p->eps_add, eps_mul_override < 0.0 ? eps_mul_override : solver_eps_mul(p),
+                                      taps, ctx, nullptr, 0.f, hg)));
     return FLR_OK;
 }
 
@@ -311,7 +316,7 @@ flr_status denoise_upsample_impl(int32_t n, int32_t Q, int32_t W_lo, int32_t H_l
     LaunchCtx ctx = make_ctx(stream, trace);
     // FUSED: the one-kernel wave schedule (flr_wave.cuh).  AUTO stays on the staged kernels:
     // on B200 the wave schedule is correct (bitwise equal) but slower
-    if (p->variant == FLR_VARIANT_FUSED && !hg) {
+    if (p->variant == FLR_VARIANT_FUSED && !hg && p->solver != FLR_SOLVER_TIKHONOV) {
         WaveLaunch W;
         W.n = n, W.W = W_lo, W.H = H_lo, W.D = D, W.U = p->upsample, W.Bx = Bx, W.By = By;
         W.G = guides_lo, W.Y = radiance_lo, W.Gout = guides_hi, W.out = out;
@@ -326,6 +331,20 @@ flr_status denoise_upsample_impl(int32_t n, int32_t Q, int32_t W_lo, int32_t H_l
     }
     if (p->variant == FLR_VARIANT_FUSED) return FLR_ERR_UNSUPPORTED;
     const int Dout = D * p->upsample;
+    if (p->solver == FLR_SOLVER_TIKHONOV && !hg) {
+        // Tikhonov models centred at the window mean, evaluated per block and blended
+        // (k_apply_centered): the raw-basis fp32 apply loses precision at eps ~1e-6
+        flr_params pc = *p;
+        const int cs = centered_stride(Q);
+        LaunchCtx* c = &ctx;
+        if ((st = do_fit(n, Q, W_lo, H_lo, guides_lo, radiance_lo, &pc, models, cs, workspace, *c, false, false,
+                         kTikhonovCentered)))
+            return st;
+        c->before("k_apply_centered");
+        FLR_DISPATCH_Q(Q, (k_apply_centered<QQ><<<dim3(cdiv(W_hi, 128), H_hi, n), 128, 0, c->s>>>(
+                               W_hi, H_hi, Dout, Bx, By, models, cs, guides_hi, out)));
+        return finish(ctx, trace);
+    }
     if (hg && (!half_guides_fit_ok(D, W_lo, guides_lo, radiance_lo) ||
                !half_guides_apply_ok(Dout, W_hi, models, guides_hi, out)))
         return FLR_ERR_UNSUPPORTED;

@@ -15,7 +15,9 @@
 #pragma once
 #include <cuda_fp16.h>
 
-#include "flr_persist.cuh"
+#include <type_traits>
+
+#include "flr_stream.cuh"
 
 namespace flr {
 
@@ -95,6 +97,61 @@ struct FitAccPix {
     }
 };
 
+// per-lane accumulators in fp64 (Tikhonov mode): its system (Mbar/n + eps I) is not
+// normalised, so at eps ~1e-6 the fp32 rounding of edge blocks' shifted sums reaches the
+// solution (model errors ~1e-3 relative at 1080p); DFMA is half the FFMA rate on B200 and
+// the fit stays bandwidth-bound.  Same interface as FitAccPix.
+template <int Q>
+struct FitAcc64 {
+    using Dm = Dims<Q>;
+    double U[Q], S[Dm::NS], Y[3], XY[3 * Q];
+    __device__ __forceinline__ void zero()
+    {
+#pragma unroll
+        for (int j = 0; j < Q; ++j) U[j] = 0.0;
+#pragma unroll
+        for (int s = 0; s < Dm::NS; ++s) S[s] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Y[c] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3 * Q; ++k) XY[k] = 0.0;
+    }
+    __device__ __forceinline__ void add(const f2 (&d2)[Q], const f2 (&y2)[3])
+    {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // the pixel pair's two pixels
+            double d[Q], y[3];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) d[j] = (double)(h ? hi2(d2[j]) : lo2(d2[j]));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) y[c] = (double)(h ? hi2(y2[c]) : lo2(y2[c]));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) Y[c] += y[c];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) U[j] += d[j];
+#pragma unroll
+            for (int i = 0; i < Q; ++i)
+#pragma unroll
+                for (int j = i; j < Q; ++j) S[Dm::s_idx(i, j) - Dm::C_S] = fma(d[i], d[j], S[Dm::s_idx(i, j) - Dm::C_S]);
+#pragma unroll
+            for (int j = 0; j < Q; ++j)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) XY[j * 3 + c] = fma(d[j], y[c], XY[j * 3 + c]);
+        }
+    }
+};
+
+// fold the m lanes of a block (xor shuffles) of fp64 sums
+template <int N>
+__device__ __forceinline__ void fold_pairs(const double (&in)[N], double (&out)[N], int m_lanes)
+{
+#pragma unroll
+    for (int k = 0; k < N; ++k) out[k] = in[k];
+    for (int m = 1; m < m_lanes; m <<= 1)
+#pragma unroll
+        for (int k = 0; k < N; ++k) out[k] += __shfl_xor_sync(0xffffffffu, out[k], m);
+}
+
 // fold the pair halves and the m lanes of a block (xor shuffles) into plain fp32 sums
 template <int N>
 __device__ __forceinline__ void fold_pairs(const f2 (&in)[N], float (&out)[N], int m_lanes)
@@ -107,8 +164,8 @@ __device__ __forceinline__ void fold_pairs(const f2 (&in)[N], float (&out)[N], i
 }
 
 // the rows of one item for one consumer warp (k: stages consumed so far by this warp)
-template <int Q, int D, bool EDGE, bool MOD, bool HG>
-__device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], const float* ring, uint64_t* full,
+template <int Q, int D, bool EDGE, bool MOD, bool HG, class Acc>
+__device__ __forceinline__ void fit_ws_rows(Acc& acc, float (&cs)[Q], const float* ring, uint64_t* full,
                                             uint64_t* empty, int& k, int rows, int lane, int lb0, int x0, int W,
                                             float afloor)
 {
@@ -175,24 +232,26 @@ __device__ __forceinline__ void fit_ws_rows(FitAccPix<Q>& acc, float (&cs)[Q], c
 // its rows from the warp's ring (k: stages consumed so far), then the epilogue -- fold the
 // pair halves and the lanes of a block, un-shift exactly to fp64 and store the moments.
 // `waited`: the grid-dependency wait has run (in early mode it runs before the first store).
-template <int Q, int D, bool MOD, bool HG>
+template <int Q, int D, bool MOD, bool HG, bool A64 = false>
 __device__ __forceinline__ void fit_consume_item(const FitArgs& a, int it, int per_frame, const float* ring,
                                                  uint64_t* full, uint64_t* empty, int& k, int lane, bool& waited)
 {
+    using Acc = std::conditional_t<A64, FitAcc64<Q>, FitAccPix<Q>>;
+    using V = std::conditional_t<A64, double, float>;
     using Dm = Dims<Q>;
     constexpr int DQ = D / kPPL;  // lanes per block
     const int f = it / per_frame, rem = it - f * per_frame, by = rem / a.nseg, sg = rem - by * a.nseg;
     const int rows = min(D, a.H - by * D);
     const int x0 = sg * kFS + lane * kPPL, bx = x0 / D, lb0 = (lane / DQ) * D;
     float cs[Q];
-    FitAccPix<Q> acc;
+    Acc acc;
     acc.zero();
     if (sg * kFS + kFS > a.W)  // segment reaches past the image
         fit_ws_rows<Q, D, true, MOD, HG>(acc, cs, ring, full, empty, k, rows, lane, lb0, x0, a.W, a.afloor);
     else
         fit_ws_rows<Q, D, false, MOD, HG>(acc, cs, ring, full, empty, k, rows, lane, lb0, x0, a.W, a.afloor);
     // epilogue: fold, then un-shift to fp64 and store (lanes of a block split the components)
-    float u[Q], sv[Dm::NS], yc[3], xy[3 * Q];
+    V u[Q], sv[Dm::NS], yc[3], xy[3 * Q];
     fold_pairs(acc.U, u, DQ);
     fold_pairs(acc.S, sv, DQ);
     fold_pairs(acc.Y, yc, DQ);
@@ -233,7 +292,7 @@ __device__ __forceinline__ void fit_consume_item(const FitArgs& a, int it, int p
     }
 }
 
-template <int Q, int D, bool MOD = false, bool HG = false>
+template <int Q, int D, bool MOD = false, bool HG = false, bool A64 = false>
 __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(const __grid_constant__ FitArgs a, int n)
 {
     using C = FitWsCfg<Q, MOD, HG>;
@@ -311,7 +370,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     int k = 0;  // stages consumed
     bool waited = !a.early;  // past the grid-dependency wait (early mode: before the first store)
     for (int it = blockIdx.x * NC + w; it < nitems; it += GW)
-        fit_consume_item<Q, D, MOD, HG>(a, it, per_frame, ring, full + w * S, empty + w * S, k, lane, waited);
+        fit_consume_item<Q, D, MOD, HG, A64>(a, it, per_frame, ring, full + w * S, empty + w * S, k, lane, waited);
     if (threadIdx.x == 0) FLR_TL(0, 2);
 }
 

@@ -5,7 +5,6 @@
 #include "flr_launch.h"
 #include "flr_staged.cuh"
 #include "flr_tiles.cuh"
-#include "flr_persist.cuh"
 #include "flr_k2.cuh"
 #include "flr_fitws.cuh"
 #include "flr_applyws.cuh"
@@ -72,7 +71,7 @@ static int num_sms()
 // K1: the warp-specialised TMA kernel when the planes allow it, else the tiled kernel
 template <int Q, int D>
 static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
-                      cudaStream_t s, const float* A, float afloor, bool hg, bool early)
+                      cudaStream_t s, const float* A, float afloor, bool hg, bool early, bool acc64)
 {
     FitArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -104,8 +103,14 @@ static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
     if (vec_ok(G, W) && vec_ok(Y, W) && make_tmap_planes(&a.tg, G, W, H, n * Q, kFS, Q, CF::RB) &&
         make_tmap_planes(&a.ty, Y, W, H, n * 3, kFS, 3, CF::RB)) {  // default: one producer warp feeds 7 consumers
         using C = CF;
+        const dim3 grid(min(num_sms(), cdiv(items, C::NC)));
+        if (acc64) {  // Tikhonov mode: fp64 accumulation (FitAcc64)
+            set_smem(k_fit_ws<Q, D, false, false, true>, C::SMEM);
+            launch_pdl(k_fit_ws<Q, D, false, false, true>, grid, dim3(C::THREADS), C::SMEM, s, a, n);
+            return;
+        }
         set_smem(k_fit_ws<Q, D>, C::SMEM);
-        launch_pdl(k_fit_ws<Q, D>, dim3(min(num_sms(), cdiv(items, C::NC))), dim3(C::THREADS), C::SMEM, s, a, n);
+        launch_pdl(k_fit_ws<Q, D>, grid, dim3(C::THREADS), C::SMEM, s, a, n);
         return;
     }
     // unaligned planes or W % 4 != 0: the tiled kernel (scalar tails)
@@ -129,10 +134,12 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     const cudaStream_t s = ctx.s;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
-        ctx.before(hg ? "k_fit_ws_f16" : A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments" : "k_fit_ws");
-        if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early);
-        else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early);
-        else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early);
+        ctx.before(hg ? "k_fit_ws_f16" : A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments"
+                   : em < 0.0 ? "k_fit_ws_f64acc" : "k_fit_ws");
+        const bool acc64 = em < 0.0 && !hg && !A;  // Tikhonov mode (flr_solve.cuh sentinels)
+        if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64);
+        else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64);
+        else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64);
     } else {
         ctx.before("k_moments_small");
         k_moments_small<Q><<<dim3(cdiv(Bx, 128), By, n), 128, 0, s>>>(W, H, Bx, By, D, G, Y, raw);
@@ -147,7 +154,9 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     // by TMA, no blurred-field round trip through L2 (flr_k2.cuh).  The tile kernel keeps
     // all KM blurred components of a block in registers, so larger Q take the row variant.
     if constexpr (Q <= 8) {
-        if (R >= 1 && R <= kTileMaxR) {
+        // (the tile stages MSTRIDE floats per block and zero-pads past the raw model, so the
+        // centred Tikhonov layout takes the row variant)
+        if (R >= 1 && R <= kTileMaxR && mstride <= Dims<Q>::MSTRIDE && !tikhonov_centered(em)) {
             const dim3 grid(cdiv(Bx, kK2TX), cdiv(By, kK2TY), n);
             bool ok = false;
 #define FLR_KT(RR)                                                                                          \
@@ -180,7 +189,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
         break;
         switch (R) { FLR_KB(1) FLR_KB(2) FLR_KB(3) FLR_KB(4) FLR_KB(5) FLR_KB(6) FLR_KB(7) FLR_KB(8) }
 #undef FLR_KB
-        if (mstride == Dims<Q>::MSTRIDE && aligned(models, 16)) {
+        if (mstride == Dims<Q>::MSTRIDE && aligned(models, 16) && !tikhonov_centered(em)) {
             ctx.before("k_solve_rows");
             set_smem(k_solve_rows<Q>, solve_rows_smem<Q>());
             launch_pdl(k_solve_rows<Q>, dim3(cdiv(Bx, kSolveRowN), By, n), dim3(kSolveRowN), solve_rows_smem<Q>(), s,
@@ -262,37 +271,23 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
     if (D % 8 == 0 && mstride == Dims<Q>::MSTRIDE && aligned(models, 16)) {
         const int off = (D / 2) % 8;
         ApplyArgs a;
-        int nsub = 1;  // sub-bands of >= 4 rows
+        int nsub = 1;  // sub-bands of >= 4 rows: finer items balance the warps of one frame
         while (D % (2 * nsub) == 0 && D / (2 * nsub) >= 4)
             nsub *= 2;
-        const int items0 = n * cdiv(W, kSeg) * apply_nband(H, D, By) * nsub;
-        const bool ring = items0 >= 4 * num_sms() * ApplyCfg<Q>::NSW;  // batches: per-warp self-feeding rings
         if (vec_ok(G, W) && vec_ok(out, W) &&
-            make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q, ring ? 1 : ApplyWsCfg<Q>::RB)) {  // TMA path
+            make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q, ApplyWsCfg<Q>::RB)) {  // TMA path
             a.models = models, a.out = out;
             a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W, kSeg), a.nband = apply_nband(H, D, By);
-            using C = ApplyCfg<Q>;
-            // sub-bands of >= 4 rows: finer items balance the warps (a single 1080p frame
-            // otherwise leaves most warps with 1 item and some with 2; measured 28 -> 25 us)
             a.nsub = nsub;
             a.reverse = 1;  // bottom-up: the fit's last rows are the likeliest still in L2
             const int items = n * a.nseg * a.nband * a.nsub;
-            // many items (batches): the 11-warp self-feeding rings keep more rows in flight;
-            // few items (one frame): the warp-specialised kernel's faster items win
-            // (measured 1080p: 1 frame 22.6 vs 26.6 us, 8 frames 17.8 vs 16.2 us per frame)
-            if (ring) {  // per-warp self-feeding rings (one row per box)
-                using C = ApplyCfg<Q>;
-                const int grid = min(num_sms(), cdiv(items, C::NSW));
-                ctx.before("k_apply_stream");
-                set_smem(k_apply_stream<Q>, C::SMEM);
-                launch_pdl(k_apply_stream<Q>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
-            } else {  // default: warp-specialised (one producer warp feeds 7 consumer warps)
-                using C = ApplyWsCfg<Q>;
-                const int grid = min(num_sms(), cdiv(items, C::NC));
-                ctx.before("k_apply_ws");
-                set_smem(k_apply_ws<Q>, C::SMEM);
-                launch_pdl(k_apply_ws<Q>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
-            }
+            // warp-specialised (one producer warp feeds 7 consumer warps, 2-row stages); faster
+            // than per-warp self-feeding rings for one frame and for batches alike
+            using C = ApplyWsCfg<Q>;
+            const int grid = min(num_sms(), cdiv(items, C::NC));
+            ctx.before("k_apply_ws");
+            set_smem(k_apply_ws<Q>, C::SMEM);
+            launch_pdl(k_apply_ws<Q>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
             return;
         }
         dim3 grid(cdiv(cdiv(W + off, 8), kApplyUnits), cdiv(H + off, kApplyRows), n),

@@ -33,7 +33,12 @@ struct SmemB {
 };
 
 template <int Q, class MomentFn, class OutT>
-__device__ __forceinline__ void solve_block_tikhonov(MomentFn&& m, double eps, OutT&& out);
+__device__ __forceinline__ void solve_block_tikhonov(MomentFn&& m, double eps, OutT&& out, bool centered = false);
+
+// eps_mul sentinels selecting the Tikhonov solve inside the library (users cannot pass a
+// negative eps_mul, flr_api.cu): raw-basis models, or models centred at the window mean
+constexpr double kTikhonovRaw = -1.0, kTikhonovCentered = -2.0;
+__host__ __device__ inline bool tikhonov_centered(double eps_mul) { return eps_mul < -1.5; }
 
 // `m(k)` returns the blurred fp64 moment component k (layout of flr_common.cuh).
 // Writes 3(Q+1) floats to `out` (row 0 = bias).  The 3 right-hand sides are solved one
@@ -43,7 +48,7 @@ template <int Q, class MomentFn, class BStore, class OutT>
 __device__ __forceinline__ void solve_block_b(MomentFn&& m, double eps_add, double eps_mul, OutT&& out, BStore& B)
 {
     if (eps_mul < 0.0) {  // Tikhonov mode sentinel (see solve_block_tikhonov)
-        solve_block_tikhonov<Q>(m, eps_add, out);
+        solve_block_tikhonov<Q>(m, eps_add, out, tikhonov_centered(eps_mul));
         return;
     }
     using Dm = Dims<Q>;
@@ -141,8 +146,12 @@ __device__ __forceinline__ void solve_block_b(MomentFn&& m, double eps_add, doub
 // system (the ones channel included, so eps also shrinks the bias), by Cholesky.
 // Selected inside the library by eps_mul < 0 (flr_params.solver = FLR_SOLVER_TIKHONOV;
 // a negative eps_mul is rejected at the ABI, so the sentinel never collides).
+// `centered`: write [b0 (3) | slopes (3Q) | mu (Q)] with mu = the window mean of the guides
+// and b0 = A0 + mu . A[1:] (in fp64), so the apply evaluates b0 + A[1:] . (x - mu): at
+// eps ~1e-6 a nearly flat guide gets slopes ~cov/eps whose raw-basis evaluation
+// A0 + A[1:] . x cancels catastrophically in fp32 (k_apply_centered).
 template <int Q, class MomentFn, class OutT>
-__device__ __forceinline__ void solve_block_tikhonov(MomentFn&& m, double eps, OutT&& out)
+__device__ __forceinline__ void solve_block_tikhonov(MomentFn&& m, double eps, OutT&& out, bool centered)
 {
     using Dm = Dims<Q>;
     constexpr int P = Q + 1, PS = P * (P + 1) / 2;
@@ -205,6 +214,22 @@ __device__ __forceinline__ void solve_block_tikhonov(MomentFn&& m, double eps, O
             c[k][cc] = v * rinv[k];
         }
     });
+    if (centered) {
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+            double b0 = c[0][cc];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) b0 = fma(c[1 + j][cc], m(Dm::C_U + j) * inv_n, b0);
+            out[cc] = (float)b0;
+        }
+#pragma unroll
+        for (int i = 1; i < P; ++i)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) out[i * 3 + cc] = (float)c[i][cc];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) out[3 * P + j] = (float)(m(Dm::C_U + j) * inv_n);
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < P; ++i)
 #pragma unroll
@@ -306,7 +331,7 @@ template <int Q, class MomentFn>
 __device__ __forceinline__ void solve_block(MomentFn&& m, double eps_add, double eps_mul, float* out)
 {
     if (eps_mul < 0.0) {  // Tikhonov mode sentinel (see solve_block_tikhonov)
-        solve_block_tikhonov<Q>(m, eps_add, out);
+        solve_block_tikhonov<Q>(m, eps_add, out, tikhonov_centered(eps_mul));
         return;
     }
 #ifdef FLR_SOLVE_NORMALISED

@@ -239,4 +239,51 @@ __global__ void __launch_bounds__(256) k_apply_px(int W, int H, int D, int Bx, i
     }
 }
 
+// K4 for Tikhonov models stored centred ([b0 | slopes | mu] per block, mstride floats,
+// solve_block_tikhonov): the four bracketing blocks' predictions b0 + A . (x - mu) are
+// evaluated separately and blended bilinearly -- equal to blending the raw models in exact
+// arithmetic (R6), but without the fp32 cancellation of large slopes against the bias.
+template <int Q>
+__global__ void __launch_bounds__(256) k_apply_centered(int W, int H, int D, int Bx, int By,
+                                                        const float* __restrict__ models, int mstride,
+                                                        const float* __restrict__ guides, float* __restrict__ out)
+{
+    constexpr int P = Q + 1;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int f = blockIdx.z;
+    if (x >= W) return;
+    const float fx = ((float)x + 0.5f) / (float)D - 0.5f;
+    const float fy = ((float)y + 0.5f) / (float)D - 0.5f;
+    const float flx = floorf(fx), fly = floorf(fy);
+    const float tx = fx - flx, ty = fy - fly;
+    const int i0 = min(max((int)flx, 0), Bx - 1), i1 = min(max((int)flx + 1, 0), Bx - 1);
+    const int j0 = min(max((int)fly, 0), By - 1), j1 = min(max((int)fly + 1, 0), By - 1);
+    const float* Mf = models + (size_t)f * By * Bx * mstride;
+    const float* A[4] = {Mf + ((size_t)j0 * Bx + i0) * mstride, Mf + ((size_t)j0 * Bx + i1) * mstride,
+                         Mf + ((size_t)j1 * Bx + i0) * mstride, Mf + ((size_t)j1 * Bx + i1) * mstride};
+    const float wgt[4] = {(1.f - tx) * (1.f - ty), tx * (1.f - ty), (1.f - tx) * ty, tx * ty};
+    const size_t plane = (size_t)W * H;
+    const size_t p = (size_t)y * W + x;
+    float xg[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) xg[q] = __ldg(guides + ((size_t)f * Q + q) * plane + p);
+    float o[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        float d[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) d[q] = xg[q] - __ldg(A[b] + 3 * P + q);
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+            float v = __ldg(A[b] + cc);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) v = fmaf(d[q], __ldg(A[b] + (1 + q) * 3 + cc), v);
+            o[cc] = fmaf(wgt[b], v, o[cc]);
+        }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) out[((size_t)f * 3 + cc) * plane + p] = o[cc];
+}
+
 }  // namespace flr

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 # (W, H, Q, frames, sigma, kernels expected in the launch list)
 CASES = [
     (640, 360, 8, 1, 10.0, ["k_fit_ws", "k_blur_solve_tile", "k_apply_ws"]),
-    (640, 360, 8, 24, 10.0, ["k_fit_ws", "k_blur_solve_tile", "k_apply_stream"]),  # batch: ring apply
+    (640, 360, 8, 24, 10.0, ["k_fit_ws", "k_blur_solve_tile", "k_apply_ws"]),  # batch
     (1000, 520, 8, 1, 20.0, ["k_blur_solve_tile"]),  # R = 5: 11-component groups
     (1032, 264, 4, 2, 10.0, ["k_fit_ws", "k_blur_solve_tile"]),  # Q = 4, edge segment
     (640, 360, 11, 1, 10.0, ["k_fit_ws", "k_blur_rows", "k_solve_rows"]),  # Q > 8: row blur

@@ -5,11 +5,12 @@ flr_params.solver = FLR_SOLVER_TIKHONOV: A = (Mbar/n + eps I)^-1 Nbar/n on the f
 and blended apply as the default path, against oracle.denoise_tikhonov on identical
 seeded inputs; bar |gpu - ref| <= 1e-5 + 1e-4 |ref|.
 
-Tikhonov models are fitted on UN-normalised guides, so at eps = 1e-6 a nearly flat guide
-(depth crowded near 1) gets slopes ~cov/1e-6 and a compensating bias; applying such a
-raw-basis model in fp32 then loses ~1e-4 relative in a handful of pixels (1080p, eps 1e-6:
-2 of 6.2 M pixels at 1.03x the bar).  The 1080p case therefore runs at eps = 1e-5; the
-appendix solver (the default) normalises and never produces such slopes.
+Tikhonov models are fitted on UN-normalised guides, so at Fig. 3's eps = 1e-6 a
+nearly flat guide (depth crowded near 1) gets slopes ~cov/1e-6 and a compensating bias;
+applying such a raw-basis model in fp32 lost ~1e-4 relative in a handful of pixels (round 1:
+2 of 6.2 M 1080p pixels at 1.03x the bar).  The denoise path now evaluates each block's
+model about its window mean and blends the four predictions (k_apply_centered), so the
+1080p case runs at eps = 1e-6.
 """
 import pytest
 import torch
@@ -30,7 +31,8 @@ def flr():
 
 
 @pytest.mark.parametrize("W,H,Q,block,sigma,eps", [
-    (1920, 1080, 8, 8, 10.0, 1e-5),   # C2 shape
+    (1920, 1080, 8, 8, 10.0, 1e-6),   # C2 shape at Fig. 3's eps
+    (1920, 1080, 8, 8, 10.0, 1e-5),
     (64, 64, 4, 8, 10.0, 1e-6),       # C1 shape, Fig. 3's eps
     (130, 66, 8, 4, 10.0, 1e-3),
     (37, 23, 3, 2, 5.0, 1e-5),        # D < 4 path, odd size
@@ -46,6 +48,7 @@ def test_tikhonov_parity(flr, oracle_mod, W, H, Q, block, sigma, eps):
     torch.cuda.synchronize()
     R = flr.effective_radius(block=block, sigma=sigma)
     ref = oracle_mod.denoise_tikhonov(G.numpy(), Y.numpy(), D=block, sigma=sigma, R=R, eps=eps)
+    assert "k_apply_centered" in flr.last_launch_names()
     rep = assert_parity(out.cpu().numpy(), ref, f"tikhonov {W}x{H} Q={Q} D={block}")
     print("tikhonov", W, H, Q, block, rep)
 
