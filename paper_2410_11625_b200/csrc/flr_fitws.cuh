@@ -25,10 +25,17 @@ namespace flr {
 #define FLR_FITWS_NC 7
 #endif
 constexpr int kFitWsNC = FLR_FITWS_NC;  // consumer warps (+1 producer = 8 warps: 2 per SMSP keeps the 255-register cap)
+#ifndef FLR_FITWS_NP
+#define FLR_FITWS_NP 1
+#endif
+constexpr int kFitWsNP = FLR_FITWS_NP;  // producer warps (producer p feeds consumers p, p + NP, ...)
 #ifndef FLR_FITWS_S
 #define FLR_FITWS_S 4
 #endif
-constexpr int kFitWsS = FLR_FITWS_S;  // ring stages per consumer
+constexpr int kFitWsS = FLR_FITWS_S;  // ring stages per consumer (1-row stages)
+#ifndef FLR_FITWS_S2
+#define FLR_FITWS_S2 2  // ring stages per consumer with 2-row stages
+#endif
 #ifndef FLR_FIT_SEG
 #define FLR_FIT_SEG 128
 #endif
@@ -47,14 +54,15 @@ struct FitWsCfg {
     // warp's issue rate, not HBM, limits one SM at one row per box (measured ~50 GB/s per
     // SM, tools/t_tma_rate.cu); two rows per box double it.  RB = 2 with 2 stages per
     // consumer when that fits in 227 KB, else single rows with up to kFitWsS stages.
-    static constexpr bool TWO = (size_t)kFitWsNC * 2 * 2 * ROWF * 4 + 4096 <= 232448;
+    static constexpr bool TWO = (size_t)kFitWsNC * FLR_FITWS_S2 * 2 * ROWF * 4 + 4096 <= 232448;
     static constexpr int RB = TWO ? 2 : 1;
     static constexpr int STG = RB * ROWF;  // floats per stage
     static constexpr int fit_stages(int s)
     {
         return (s <= 2 || (size_t)kFitWsNC * s * STG * 4 + 4096 <= 232448) ? s : fit_stages(s - 1);
     }
-    static constexpr int NC = kFitWsNC, S = TWO ? 2 : fit_stages(kFitWsS), THREADS = (NC + 1) * 32;
+    static constexpr int NC = kFitWsNC, NP = kFitWsNP, S = TWO ? FLR_FITWS_S2 : fit_stages(kFitWsS),
+                         THREADS = (NC + NP) * 32;
     static constexpr size_t BAR_OFF = (size_t)NC * S * STG * sizeof(float);
     static constexpr size_t SMEM = BAR_OFF + 2 * NC * S * sizeof(uint64_t);
     static_assert(SMEM <= 232448, "fit pipeline exceeds 227 KB of shared memory");
@@ -324,10 +332,11 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
     }
     if (threadIdx.x == 0) FLR_TL(0, 1);
 
-    if (warp == NC) {
-        // ---------------- producer: lane c feeds consumer c ----------------
-        if (lane >= NC) return;
-        const int c = lane;
+    if (warp >= NC) {
+        // ---------------- producer p: lane i feeds consumer c = p + NP i ----------------
+        constexpr int NP = C::NP, LANES = (NC + NP - 1) / NP;
+        const int p = warp - NC, c = p + NP * lane;
+        if (lane >= LANES || c >= NC) return;
         const uint64_t pg = policy_evict_first(), py = policy_evict_first();
         int it = blockIdx.x * NC + c, row = 0, rows = 0, f = 0, by = 0, sg = 0;
         auto decode = [&]() {
@@ -339,10 +348,10 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
             rows = min(D, a.H - by * D);
         };
         decode();
-        // the NC lanes stay converged: each round, every lane whose next slot is free
-        // (non-blocking test) issues one row for its consumer
+        // the lanes stay converged: each round, every lane whose next slot is free
+        // (non-blocking test) issues one stage for its consumer
         int k = 0;
-        constexpr unsigned mask = (1u << NC) - 1;
+        const unsigned mask = __activemask();
         while (__any_sync(mask, it < nitems)) {
             const int slot = k % S;
             if (it < nitems && (k < S || mbar_test_wait(&empty[c * S + slot], ((k / S) - 1) & 1))) {
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
                 }
             }
         }
-        if (a.early && lane == 0) {
+        if (a.early && lane == 0) {  // (each trigger follows a completed wait: safe from any producer)
             pdl_wait();
             pdl_trigger();
         }
