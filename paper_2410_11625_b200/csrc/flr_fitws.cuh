@@ -172,10 +172,11 @@ __device__ __forceinline__ void fold_pairs(const f2 (&in)[N], float (&out)[N], i
 }
 
 // the rows of one item for one consumer warp (k: stages consumed so far by this warp)
-template <int Q, int D, bool EDGE, bool MOD, bool HG, class Acc>
-__device__ __forceinline__ void fit_ws_rows(Acc& acc, float (&cs)[Q], const float* ring, uint64_t* full,
-                                            uint64_t* empty, int& k, int rows, int lane, int lb0, int x0, int W,
-                                            float afloor)
+// Rel: called by lane 0 with the slot once its values are in registers (frees the stage:
+// arrive on its `empty` barrier, or -- self-feeding warps -- issue the next stage into it)
+template <int Q, int D, bool EDGE, bool MOD, bool HG, class Acc, class Rel>
+__device__ __forceinline__ void fit_ws_rows(Acc& acc, float (&cs)[Q], const float* ring, uint64_t* full, Rel&& rel,
+                                            int& k, int rows, int lane, int lb0, int x0, int W, float afloor)
 {
     using C = FitWsCfg<Q, MOD, HG>;
     constexpr int S = C::S, STG = C::STG, RB = C::RB;
@@ -232,7 +233,7 @@ __device__ __forceinline__ void fit_ws_rows(Acc& acc, float (&cs)[Q], const floa
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);  // values are in registers: free the stage
+        if (lane == 0) rel(slot);  // values are in registers: free the stage
     }
 }
 
@@ -240,9 +241,9 @@ __device__ __forceinline__ void fit_ws_rows(Acc& acc, float (&cs)[Q], const floa
 // its rows from the warp's ring (k: stages consumed so far), then the epilogue -- fold the
 // pair halves and the lanes of a block, un-shift exactly to fp64 and store the moments.
 // `waited`: the grid-dependency wait has run (in early mode it runs before the first store).
-template <int Q, int D, bool MOD, bool HG, bool A64 = false>
-__device__ __forceinline__ void fit_consume_item(const FitArgs& a, int it, int per_frame, const float* ring,
-                                                 uint64_t* full, uint64_t* empty, int& k, int lane, bool& waited)
+template <int Q, int D, bool MOD, bool HG, bool A64, class Rel>
+__device__ __forceinline__ void fit_consume_item_rel(const FitArgs& a, int it, int per_frame, const float* ring,
+                                                     uint64_t* full, Rel&& rel, int& k, int lane, bool& waited)
 {
     using Acc = std::conditional_t<A64, FitAcc64<Q>, FitAccPix<Q>>;
     using V = std::conditional_t<A64, double, float>;
@@ -255,9 +256,9 @@ __device__ __forceinline__ void fit_consume_item(const FitArgs& a, int it, int p
     Acc acc;
     acc.zero();
     if (sg * kFS + kFS > a.W)  // segment reaches past the image
-        fit_ws_rows<Q, D, true, MOD, HG>(acc, cs, ring, full, empty, k, rows, lane, lb0, x0, a.W, a.afloor);
+        fit_ws_rows<Q, D, true, MOD, HG>(acc, cs, ring, full, rel, k, rows, lane, lb0, x0, a.W, a.afloor);
     else
-        fit_ws_rows<Q, D, false, MOD, HG>(acc, cs, ring, full, empty, k, rows, lane, lb0, x0, a.W, a.afloor);
+        fit_ws_rows<Q, D, false, MOD, HG>(acc, cs, ring, full, rel, k, rows, lane, lb0, x0, a.W, a.afloor);
     // epilogue: fold, then un-shift to fp64 and store (lanes of a block split the components)
     V u[Q], sv[Dm::NS], yc[3], xy[3 * Q];
     fold_pairs(acc.U, u, DQ);
@@ -300,6 +301,13 @@ __device__ __forceinline__ void fit_consume_item(const FitArgs& a, int it, int p
     }
 }
 
+template <int Q, int D, bool MOD, bool HG, bool A64 = false>
+__device__ __forceinline__ void fit_consume_item(const FitArgs& a, int it, int per_frame, const float* ring,
+                                                 uint64_t* full, uint64_t* empty, int& k, int lane, bool& waited)
+{
+    fit_consume_item_rel<Q, D, MOD, HG, A64>(a, it, per_frame, ring, full, [&](int s) { mbar_arrive(&empty[s]); }, k,
+                                             lane, waited);
+}
 template <int Q, int D, bool MOD = false, bool HG = false, bool A64 = false>
 __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(const __grid_constant__ FitArgs a, int n)
 {
@@ -382,5 +390,6 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
         fit_consume_item<Q, D, MOD, HG, A64>(a, it, per_frame, ring, full + w * S, empty + w * S, k, lane, waited);
     if (threadIdx.x == 0) FLR_TL(0, 2);
 }
+
 
 }  // namespace flr

@@ -7,6 +7,76 @@
 #include "../paper_2410_11625_b200/csrc/flr_launch.h"
 #include "../paper_2410_11625_b200/csrc/flr_fitws.cuh"
 #include "../paper_2410_11625_b200/csrc/flr_applyws.cuh"
+namespace flr {
+// K1 with self-feeding consumer warps (experiment): no producer warp; lane 0
+// of each of kFitSelfW warps issues its own 2-row stages, the next one into the slot it has
+// just read, so a stage's round trip is the TMA latency alone.
+#ifndef FLR_FITSELF_W
+#define FLR_FITSELF_W 8
+#endif
+#ifndef FLR_FITSELF_S
+#define FLR_FITSELF_S 2
+#endif
+constexpr int kFitSelfW = FLR_FITSELF_W, kFitSelfS = FLR_FITSELF_S;
+template <int Q>
+struct FitSelfCfg {
+    using FC = FitWsCfg<Q>;
+    static constexpr int STG = FC::STG, S = kFitSelfS, NW = kFitSelfW, THREADS = NW * 32;
+    static constexpr size_t BAR_OFF = (size_t)NW * S * STG * sizeof(float);
+    static constexpr size_t SMEM = BAR_OFF + NW * S * sizeof(uint64_t);
+    static_assert(SMEM <= 232448, "self-feeding fit exceeds 227 KB of shared memory");
+};
+template <int Q, int D>
+__global__ void __launch_bounds__(FitSelfCfg<Q>::THREADS, 1) k_fit_self(const __grid_constant__ FitArgs a, int n)
+{
+    using C = FitSelfCfg<Q>;
+    using FC = FitWsCfg<Q>;
+    constexpr int S = C::S, STG = C::STG, NW = C::NW, RB = FC::RB;
+    static_assert(FC::S == S || true, "");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* ring = reinterpret_cast<float*>(smem_raw) + (size_t)w * S * STG;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF) + w * S;
+    if (lane == 0) {
+        for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_trigger();
+    const int per_frame = a.By * a.nseg, nitems = n * per_frame, GW = gridDim.x * NW;
+    const uint64_t pg = policy_evict_first(), py = policy_evict_first();
+    int pit = blockIdx.x * NW + w, prow = 0, prows = 0, pf = 0, pby = 0, psg = 0;  // issue cursor (lane 0)
+    auto decode = [&]() {
+        if (pit >= nitems) return;
+        pf = pit / per_frame;
+        const int rem = pit - pf * per_frame;
+        pby = rem / a.nseg;
+        psg = rem - pby * a.nseg;
+        prows = min(D, a.H - pby * D);
+    };
+    auto issue = [&](int slot) {
+        if (pit >= nitems) return;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        fit_issue_row<Q, D, false, false, kFS, RB>(a, pf, pby, psg, prow, ring + slot * STG, &full[slot], pg, py);
+        if ((prow += RB) >= prows) {
+            prow = 0;
+            pit += GW;
+            decode();
+        }
+    };
+    if (lane == 0) {
+        decode();
+        for (int s = 0; s < S; ++s) issue(s);
+    }
+    __syncwarp();
+    int k = 0;
+    bool waited = true;
+    for (int it = blockIdx.x * NW + w; it < nitems; it += GW)
+        fit_consume_item_rel<Q, D, false, false, false>(a, it, per_frame, ring, full, issue, k, lane, waited);
+}
+
+}  // namespace flr
 using namespace flr;
 int main()
 {
@@ -51,6 +121,20 @@ int main()
             cudaEventElapsedTime(&ms, e0, e1);
         }
         const double tf = 1e-3 * ms / reps;
+        double tself = 0;
+        {
+            using SC = FitSelfCfg<Q>;
+            static bool once = false;
+            if (!once) cudaFuncSetAttribute(k_fit_self<Q, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SC::SMEM), once = true;
+            for (int k = 0; k < 2; ++k) {
+                cudaEventRecord(e0);
+                for (int r = 0; r < reps; ++r) k_fit_self<Q, D><<<g, SC::THREADS, SC::SMEM>>>(fa, nf);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                cudaEventElapsedTime(&ms, e0, e1);
+            }
+            tself = 1e-3 * ms / reps;
+        }
         for (int k = 0; k < 2; ++k) {
             cudaEventRecord(e0);
             for (int r = 0; r < reps; ++r) k_apply_ws<Q><<<g, AC::THREADS, AC::SMEM>>>(aa, nf);
@@ -59,8 +143,9 @@ int main()
             cudaEventElapsedTime(&ms, e0, e1);
         }
         const double ta = 1e-3 * ms / reps;
-        printf("G=%3d  fit %7.2f us/frame %6.0f GB/s (%5.1f GB/s/SM)   apply %7.2f us/frame %6.0f GB/s (%5.1f GB/s/SM)  %s\n",
-               g, 1e6 * tf / nf, fit_bytes / tf / 1e9, fit_bytes / tf / 1e9 / g, 1e6 * ta / nf, app_bytes / ta / 1e9,
+        printf("G=%3d  fit %7.2f us/frame %6.0f GB/s (%5.1f GB/s/SM)  self-fed fit %7.2f us/frame (%5.1f GB/s/SM)   apply %7.2f us/frame %6.0f GB/s (%5.1f GB/s/SM)  %s\n",
+               g, 1e6 * tf / nf, fit_bytes / tf / 1e9, fit_bytes / tf / 1e9 / g, 1e6 * tself / nf, fit_bytes / tself / 1e9 / g,
+               1e6 * ta / nf, app_bytes / ta / 1e9,
                app_bytes / ta / 1e9 / g, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
