@@ -180,14 +180,17 @@ __global__ void __launch_bounds__(128) k_vblur_solve(int Bx, int Bxp, int By, co
     const size_t cs = (size_t)Bxp * By;
     const double* base = hb + (size_t)f * Dm::KM * cs + bx;
     const int lo = max(-t.R, -by), hi = min(t.R, By - 1 - by);
-    auto vb = [&](int k) -> double {
+    // every component's vertical pass once, then the solve on the values (an on-the-fly
+    // blur inside the solve's component accessor unrolled into ~40 K instructions)
+    double vb[Dm::KM];
+#pragma unroll 1
+    for (int k = 0; k < Dm::KM; ++k) {
         const double* src = base + (size_t)k * cs;
         double acc = 0.0;
         for (int d = lo; d <= hi; ++d) acc = fma(t.g[t.R + d], __ldg(src + (size_t)(by + d) * Bxp), acc);
-        return acc;
-    };
-
-    solve_block<Q>(vb, eps_add, eps_mul, models + ((size_t)(f * By + by) * Bx + bx) * mstride);
+        vb[k] = acc;
+    }
+    solve_block<Q>([&](int k) { return vb[k]; }, eps_add, eps_mul, models + ((size_t)(f * By + by) * Bx + bx) * mstride);
 }
 
 // ---------------------------------------------------------------------------
