@@ -161,14 +161,14 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
             bool ok = false;
 #define FLR_KT(RR)                                                                                          \
     case RR: {                                                                                              \
-        using KG = K2Geom<Q, RR>;                                                                           \
+        using KG = K2WsGeom<Q, RR>;                                                                         \
         if (!make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, KG::HX, \
                           KG::NV, KG::G))                                                                   \
             break;                                                                                          \
         ctx.before("k_blur_solve_tile");                                                                    \
         set_smem(k_blur_solve_tile<Q, RR>, KG::SMEM);                                                       \
-        launch_pdl(k_blur_solve_tile<Q, RR>, grid, dim3(kK2Threads), KG::SMEM, s, tm, Bx, By, models, mstride, \
-                   ea, em, taps);                                                                           \
+        launch_pdl(k_blur_solve_tile<Q, RR>, grid, dim3(kK2WsThreads), KG::SMEM, s, tm, Bx, By, models, mstride, \
+                   ea, em, taps);                                                                  \
         ok = true;                                                                                          \
         break;                                                                                              \
     }

@@ -204,6 +204,12 @@ __device__ __forceinline__ void red_release_add(int* p, int v)
 
 namespace flr {
 
+// named barrier `id` (1..15) over `count` threads (a multiple of 32) of the CTA
+__device__ __forceinline__ void named_bar_sync(int id, int count)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // ---- programmatic dependent launch (no-ops when launched without the PDL attribute) ----
 // wait: block until the preceding grid in the stream has completed and flushed its writes
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -150,91 +150,204 @@ __device__ __forceinline__ void solve_block_b(MomentFn&& m, double eps_add, doub
 // and b0 = A0 + mu . A[1:] (in fp64), so the apply evaluates b0 + A[1:] . (x - mu): at
 // eps ~1e-6 a nearly flat guide gets slopes ~cov/eps whose raw-basis evaluation
 // A0 + A[1:] . x cancels catastrophically in fp32 (k_apply_centered).
+// Two phases, so a caller that receives the blurred components in order (n, u, S, Y, then
+// XY: flr_common.cuh) can factor the system before the cross moments arrive (flr_k2.cuh):
+// factor() reads components [0, C_XY), finish() the rest.
+template <int Q>
+struct TikhonovSolve {
+    static constexpr int P = Q + 1, PS = P * (P + 1) / 2;
+    __device__ static constexpr int at(int i, int j) { return i * P - (i * (i - 1)) / 2 + (j - i); }  // i <= j
+    double inv_n, T[PS], rinv[P], mu[Q];
+    template <class MomentFn>
+    __device__ __forceinline__ void factor(MomentFn&& m, double eps)
+    {
+        using Dm = Dims<Q>;
+        inv_n = 1.0 / m(Dm::C_N);
+        T[at(0, 0)] = 1.0 + eps;
+#pragma unroll
+        for (int j = 0; j < Q; ++j) mu[j] = m(Dm::C_U + j) * inv_n;
+#pragma unroll
+        for (int j = 0; j < Q; ++j) T[at(0, 1 + j)] = mu[j];
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+            for (int j = i; j < Q; ++j) T[at(1 + i, 1 + j)] = fma(m(Dm::s_idx(i, j)), inv_n, i == j ? eps : 0.0);
+        static_for<P>([&](auto K) {
+            constexpr int k = decltype(K)::value;
+            double dkk = T[at(k, k)];
+            static_for<k>([&](auto PP) {
+                constexpr int p = decltype(PP)::value;
+                dkk = fma(-T[at(p, k)], T[at(p, k)], dkk);
+            });
+            rinv[k] = rsqrt(dkk);
+            static_for<P - k - 1>([&](auto JJ) {
+                constexpr int j = k + 1 + decltype(JJ)::value;
+                double v = T[at(k, j)];
+                static_for<k>([&](auto PP) {
+                    constexpr int p = decltype(PP)::value;
+                    v = fma(-T[at(p, k)], T[at(p, j)], v);
+                });
+                T[at(k, j)] = v * rinv[k];
+            });
+        });
+    }
+    template <class MomentFn, class OutT>
+    __device__ __forceinline__ void finish(MomentFn&& m, OutT&& out, bool centered)
+    {
+        using Dm = Dims<Q>;
+        double c[P][3];
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) c[0][cc] = m(Dm::C_Y + cc) * inv_n;
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) c[1 + i][cc] = m(Dm::C_XY + i * 3 + cc) * inv_n;
+        static_for<P>([&](auto K) {
+            constexpr int k = decltype(K)::value;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                double v = c[k][cc];
+                static_for<k>([&](auto PP) {
+                    constexpr int p = decltype(PP)::value;
+                    v = fma(-T[at(p, k)], c[p][cc], v);
+                });
+                c[k][cc] = v * rinv[k];
+            }
+        });
+        static_for<P>([&](auto KK) {
+            constexpr int k = P - 1 - decltype(KK)::value;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                double v = c[k][cc];
+                static_for<P - 1 - k>([&](auto PP) {
+                    constexpr int p = k + 1 + decltype(PP)::value;
+                    v = fma(-T[at(k, p)], c[p][cc], v);
+                });
+                c[k][cc] = v * rinv[k];
+            }
+        });
+        if (centered) {
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                double b0 = c[0][cc];
+#pragma unroll
+                for (int j = 0; j < Q; ++j) b0 = fma(c[1 + j][cc], mu[j], b0);
+                out[cc] = (float)b0;
+            }
+#pragma unroll
+            for (int i = 1; i < P; ++i)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) out[i * 3 + cc] = (float)c[i][cc];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) out[3 * P + j] = (float)mu[j];
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) out[i * 3 + cc] = (float)c[i][cc];
+    }
+};
+
 template <int Q, class MomentFn, class OutT>
 __device__ __forceinline__ void solve_block_tikhonov(MomentFn&& m, double eps, OutT&& out, bool centered)
 {
-    using Dm = Dims<Q>;
-    constexpr int P = Q + 1, PS = P * (P + 1) / 2;
-    auto at = [](int i, int j) { return i * P - (i * (i - 1)) / 2 + (j - i); };  // i <= j
-    const double inv_n = 1.0 / m(Dm::C_N);
-    double T[PS], c[P][3];
-    T[at(0, 0)] = 1.0 + eps;
-#pragma unroll
-    for (int j = 0; j < Q; ++j) T[at(0, 1 + j)] = m(Dm::C_U + j) * inv_n;
-#pragma unroll
-    for (int i = 0; i < Q; ++i)
-#pragma unroll
-        for (int j = i; j < Q; ++j) T[at(1 + i, 1 + j)] = fma(m(Dm::s_idx(i, j)), inv_n, i == j ? eps : 0.0);
-#pragma unroll
-    for (int cc = 0; cc < 3; ++cc) c[0][cc] = m(Dm::C_Y + cc) * inv_n;
-#pragma unroll
-    for (int i = 0; i < Q; ++i)
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) c[1 + i][cc] = m(Dm::C_XY + i * 3 + cc) * inv_n;
-    double rinv[P];
-    static_for<P>([&](auto K) {
-        constexpr int k = decltype(K)::value;
-        double dkk = T[at(k, k)];
-        static_for<k>([&](auto PP) {
-            constexpr int p = decltype(PP)::value;
-            dkk = fma(-T[at(p, k)], T[at(p, k)], dkk);
-        });
-        rinv[k] = rsqrt(dkk);
-        static_for<P - k - 1>([&](auto JJ) {
-            constexpr int j = k + 1 + decltype(JJ)::value;
-            double v = T[at(k, j)];
-            static_for<k>([&](auto PP) {
-                constexpr int p = decltype(PP)::value;
-                v = fma(-T[at(p, k)], T[at(p, j)], v);
-            });
-            T[at(k, j)] = v * rinv[k];
-        });
-    });
-    static_for<P>([&](auto K) {
-        constexpr int k = decltype(K)::value;
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-            double v = c[k][cc];
-            static_for<k>([&](auto PP) {
-                constexpr int p = decltype(PP)::value;
-                v = fma(-T[at(p, k)], c[p][cc], v);
-            });
-            c[k][cc] = v * rinv[k];
-        }
-    });
-    static_for<P>([&](auto KK) {
-        constexpr int k = P - 1 - decltype(KK)::value;
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-            double v = c[k][cc];
-            static_for<P - 1 - k>([&](auto PP) {
-                constexpr int p = k + 1 + decltype(PP)::value;
-                v = fma(-T[at(k, p)], c[p][cc], v);
-            });
-            c[k][cc] = v * rinv[k];
-        }
-    });
-    if (centered) {
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-            double b0 = c[0][cc];
-#pragma unroll
-            for (int j = 0; j < Q; ++j) b0 = fma(c[1 + j][cc], m(Dm::C_U + j) * inv_n, b0);
-            out[cc] = (float)b0;
-        }
-#pragma unroll
-        for (int i = 1; i < P; ++i)
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) out[i * 3 + cc] = (float)c[i][cc];
-#pragma unroll
-        for (int j = 0; j < Q; ++j) out[3 * P + j] = (float)(m(Dm::C_U + j) * inv_n);
-        return;
-    }
-#pragma unroll
-    for (int i = 0; i < P; ++i)
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) out[i * 3 + cc] = (float)c[i][cc];
+    TikhonovSolve<Q> t;
+    t.factor(m, eps);
+    t.finish(m, out, centered);
 }
+
+// In two phases like TikhonovSolve: factor() reads [0, C_XY), finish() the cross moments.
+template <int Q>
+struct DirectSolve {
+    using Dm = Dims<Q>;
+    double inv_n, mu[Q], M[Dm::NS], rinv[Q], muY[3];
+    template <class MomentFn>
+    __device__ __forceinline__ void factor(MomentFn&& m, double eps_add, double eps_mul)
+    {
+        inv_n = 1.0 / m(Dm::C_N);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) mu[j] = m(Dm::C_U + j) * inv_n;
+        const double om = 1.0 - eps_mul;
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+            for (int j = i; j < Q; ++j) {
+                double w = fma(m(Dm::s_idx(i, j)), inv_n, -om * mu[i] * mu[j]);
+                if (i == j) {
+                    w += fma(eps_mul * mu[i], mu[i], eps_add);          // W^_ii
+                    w = fma(eps_add, fmax(w, 1e-300), w);                // + eps sigma^_i^2
+                }
+                M[Dm::s_idx(i, j) - Dm::C_S] = w;
+            }
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) muY[cc] = m(Dm::C_Y + cc) * inv_n;
+        // Cholesky M = R^T R (R upper, in place)
+        static_for<Q>([&](auto K) {
+            constexpr int k = decltype(K)::value;
+            double dkk = M[Dm::s_idx(k, k) - Dm::C_S];
+            static_for<k>([&](auto PP) {
+                constexpr int p = decltype(PP)::value;
+                const double r = M[Dm::s_idx(p, k) - Dm::C_S];
+                dkk = fma(-r, r, dkk);
+            });
+            rinv[k] = rsqrt(dkk);
+            static_for<Q - k - 1>([&](auto JJ) {
+                constexpr int j = k + 1 + decltype(JJ)::value;
+                double v = M[Dm::s_idx(k, j) - Dm::C_S];
+                static_for<k>([&](auto PP) {
+                    constexpr int p = decltype(PP)::value;
+                    v = fma(-M[Dm::s_idx(p, k) - Dm::C_S], M[Dm::s_idx(p, j) - Dm::C_S], v);
+                });
+                M[Dm::s_idx(k, j) - Dm::C_S] = v * rinv[k];
+            });
+        });
+    }
+    template <class MomentFn, class OutT>
+    __device__ __forceinline__ void finish(MomentFn&& m, OutT&& out)
+    {
+        double c[Q][3];
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) c[i][cc] = fma(m(Dm::C_XY + i * 3 + cc), inv_n, -mu[i] * muY[cc]);
+        // R^T z = c, R a = z (3 channels interleaved), raw model
+        static_for<Q>([&](auto K) {
+            constexpr int k = decltype(K)::value;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                double v = c[k][cc];
+                static_for<k>([&](auto PP) {
+                    constexpr int p = decltype(PP)::value;
+                    v = fma(-M[Dm::s_idx(p, k) - Dm::C_S], c[p][cc], v);
+                });
+                c[k][cc] = v * rinv[k];
+            }
+        });
+        static_for<Q>([&](auto KK) {
+            constexpr int k = Q - 1 - decltype(KK)::value;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                double v = c[k][cc];
+                static_for<Q - 1 - k>([&](auto PP) {
+                    constexpr int p = k + 1 + decltype(PP)::value;
+                    v = fma(-M[Dm::s_idx(k, p) - Dm::C_S], c[p][cc], v);
+                });
+                c[k][cc] = v * rinv[k];
+            }
+        });
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+            double bias = muY[cc];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) {
+                out[(1 + j) * 3 + cc] = (float)c[j][cc];
+                bias = fma(-mu[j], c[j][cc], bias);
+            }
+            out[cc] = (float)bias;
+        }
+    }
+};
 
 // The same solution without forming C^ (R13: any exact solve of the same system).  With
 // D = diag(sigma^) (sigma^_i^2 = max(W^_ii, 1e-300)), C^ + eps I = D^-1 (W^ + eps D^2) D^-1
@@ -244,87 +357,9 @@ __device__ __forceinline__ void solve_block_tikhonov(MomentFn&& m, double eps, O
 template <int Q, class MomentFn, class OutT>
 __device__ __forceinline__ void solve_block_direct(MomentFn&& m, double eps_add, double eps_mul, OutT&& out)
 {
-    using Dm = Dims<Q>;
-    const double inv_n = 1.0 / m(Dm::C_N);
-    double mu[Q];
-#pragma unroll
-    for (int j = 0; j < Q; ++j) mu[j] = m(Dm::C_U + j) * inv_n;
-    double M[Dm::NS];
-    const double om = 1.0 - eps_mul;
-#pragma unroll
-    for (int i = 0; i < Q; ++i)
-#pragma unroll
-        for (int j = i; j < Q; ++j) {
-            double w = fma(m(Dm::s_idx(i, j)), inv_n, -om * mu[i] * mu[j]);
-            if (i == j) {
-                w += fma(eps_mul * mu[i], mu[i], eps_add);          // W^_ii
-                w = fma(eps_add, fmax(w, 1e-300), w);                // + eps sigma^_i^2
-            }
-            M[Dm::s_idx(i, j) - Dm::C_S] = w;
-        }
-    double muY[3], c[Q][3];
-#pragma unroll
-    for (int cc = 0; cc < 3; ++cc) muY[cc] = m(Dm::C_Y + cc) * inv_n;
-#pragma unroll
-    for (int i = 0; i < Q; ++i)
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) c[i][cc] = fma(m(Dm::C_XY + i * 3 + cc), inv_n, -mu[i] * muY[cc]);
-    // Cholesky M = R^T R (R upper, in place)
-    double rinv[Q];
-    static_for<Q>([&](auto K) {
-        constexpr int k = decltype(K)::value;
-        double dkk = M[Dm::s_idx(k, k) - Dm::C_S];
-        static_for<k>([&](auto PP) {
-            constexpr int p = decltype(PP)::value;
-            const double r = M[Dm::s_idx(p, k) - Dm::C_S];
-            dkk = fma(-r, r, dkk);
-        });
-        rinv[k] = rsqrt(dkk);
-        static_for<Q - k - 1>([&](auto JJ) {
-            constexpr int j = k + 1 + decltype(JJ)::value;
-            double v = M[Dm::s_idx(k, j) - Dm::C_S];
-            static_for<k>([&](auto PP) {
-                constexpr int p = decltype(PP)::value;
-                v = fma(-M[Dm::s_idx(p, k) - Dm::C_S], M[Dm::s_idx(p, j) - Dm::C_S], v);
-            });
-            M[Dm::s_idx(k, j) - Dm::C_S] = v * rinv[k];
-        });
-    });
-    // R^T z = c, R a = z (3 channels interleaved), raw model
-    static_for<Q>([&](auto K) {
-        constexpr int k = decltype(K)::value;
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-            double v = c[k][cc];
-            static_for<k>([&](auto PP) {
-                constexpr int p = decltype(PP)::value;
-                v = fma(-M[Dm::s_idx(p, k) - Dm::C_S], c[p][cc], v);
-            });
-            c[k][cc] = v * rinv[k];
-        }
-    });
-    static_for<Q>([&](auto KK) {
-        constexpr int k = Q - 1 - decltype(KK)::value;
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-            double v = c[k][cc];
-            static_for<Q - 1 - k>([&](auto PP) {
-                constexpr int p = k + 1 + decltype(PP)::value;
-                v = fma(-M[Dm::s_idx(k, p) - Dm::C_S], c[p][cc], v);
-            });
-            c[k][cc] = v * rinv[k];
-        }
-    });
-#pragma unroll
-    for (int cc = 0; cc < 3; ++cc) {
-        double bias = muY[cc];
-#pragma unroll
-        for (int j = 0; j < Q; ++j) {
-            out[(1 + j) * 3 + cc] = (float)c[j][cc];
-            bias = fma(-mu[j], c[j][cc], bias);
-        }
-        out[cc] = (float)bias;
-    }
+    DirectSolve<Q> d;
+    d.factor(m, eps_add, eps_mul);
+    d.finish(m, out);
 }
 
 template <int Q, class MomentFn>

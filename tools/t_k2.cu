@@ -53,7 +53,7 @@ int main(int argc, char** argv)
         cudaEventElapsedTime(&tsv, e[1], e[2]);
     }
     {
-        using KG = K2Geom<Q, R>;
+        using KG = K2WsGeom<Q, R>;
         cudaFuncSetAttribute(k_blur_solve_tile<Q, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KG::SMEM);
         const dim3 gt(cdiv(Bx, kK2TX), cdiv(By, kK2TY), n);
         CUtensorMap tmk;
@@ -61,7 +61,7 @@ int main(int argc, char** argv)
         float tt = 0;
         for (int rep = 0; rep < 2000; ++rep) {
             if (rep == 1990) cudaEventRecord(e[0]);
-            k_blur_solve_tile<Q, R><<<gt, kK2Threads, KG::SMEM>>>(tmk, Bx, By, models, Dims<Q>::MSTRIDE, 1e-5, 1e-4, t);
+            k_blur_solve_tile<Q, R><<<gt, kK2WsThreads, KG::SMEM>>>(tmk, Bx, By, models, Dims<Q>::MSTRIDE, 1e-5, 1e-4, t);
         }
         cudaEventRecord(e[1]);
         cudaEventSynchronize(e[1]);
