@@ -163,7 +163,7 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
     case RR: {                                                                                              \
         using KG = K2WsGeom<Q, RR>;                                                                         \
         if (!make_tmap_3d(&tm, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * Dims<Q>::KM, KG::HX, \
-                          KG::NV, KG::G))                                                                   \
+                          KG::NVB, KG::G))                                                                   \
             break;                                                                                          \
         ctx.before("k_blur_solve_tile");                                                                    \
         set_smem(k_blur_solve_tile<Q, RR>, KG::SMEM);                                                       \
@@ -323,7 +323,7 @@ bool launch_wave(const WaveLaunch& L, LaunchCtx& ctx)
     auto tmom = [&](auto KGv) {
         using KG = decltype(KGv);
         return make_tmap_3d(&w.tmom, L.mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, L.Bx, L.By, Bxp, L.n * Dims<Q>::KM, KG::HX,
-                            KG::NV, KG::G);
+                            KG::NVB, KG::G);
     };
     if (!(R == 3 ? tmom(K2Geom<Q, 3>{}) : tmom(K2Geom<Q, 5>{}))) return false;
     w.fit.mom = L.mom;

@@ -39,32 +39,50 @@ constexpr int kK2BlurThreads = 32 * FLR_K2_BLUR_WARPS, kK2WsThreads = kK2Threads
 // WS: the geometry of the warp-specialised kernel (k_blur_solve_tile): NST = 2 stages
 // between the blur and the solve warps, G reduced until everything fits in 227 KB, and
 // 8-column h-pass tasks (bank-conflict free; the 128 blur threads have tasks to spare).
+// model staging stride in shared memory: MSTRIDE + 1 floats (odd: the solve threads' stores
+// of one model component fall on 32 distinct banks)
+template <int Q>
+constexpr int k2_msp = Dims<Q>::MSTRIDE + 1;
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
 template <int Q, int R, bool WS = false>
 struct K2Geom {
     static constexpr int RE = (R + 1) & ~1;     // x halo, even: 16-byte aligned pairs in vb
     static constexpr int HX = kK2TX + 2 * RE;   // halo columns
     static constexpr int NV = kK2TY + 2 * R;    // values per v-pass column task
+    // TMA box rows: NV + 1 where that makes the box's plane pitch HX * NVB = HX (mod 16
+    // doubles): a half warp of v-pass lanes crossing from one plane's last columns into the
+    // next plane's first then still hits 16 distinct 8-byte bank pairs (R = 3, 4)
+    static constexpr int NVB = (HX * (NV - 1)) % 16 != 0 && (HX * NV) % 16 == 0 ? NV + 1 : NV;
     static constexpr int VT = R <= 5 ? 2 : 1;   // v-pass column tasks per thread (256 threads)
     static constexpr int S = VT == 2 ? 2 : 3;   // TMA ring stages
     static constexpr int NST = WS ? 2 : 1;      // blur -> solve stages
-    // vb: [G][TY][VP], halo column u at u + 2 (u / 8); stage: [G][TY][SP], column x at
-    // x + 2 (x / 8).  Pitches = 8 (mod 16) doubles: the h-pass's 16-byte accesses of the
-    // 8 lanes of a quarter warp then fall on distinct bank groups.
-    static constexpr int VPMIN = HX + 2 * ((HX - 1) / 8);
-    static constexpr int VP = ((VPMIN - 8 + 15) / 16) * 16 + 8;
-    static constexpr int SP = 40;
+    // vb: [G] planes of pitch PV, row r at r VP, halo column u at u; stage: [G][TY][SP].
+    // Shared-memory bank rules (8-byte accesses: 16 lanes per wavefront; 16-byte: 8):
+    //  * row pitches VP, SP = 2 (mod 4) doubles: the h-pass's quarter warps (8 rows of one
+    //    column chunk) then read vb and write the stage on 8 distinct 16-byte bank groups;
+    //  * rows hold their columns contiguously: the v-pass stores and the gather (consecutive
+    //    columns per lane) are conflict free;
+    //  * plane pitch PV = HX (mod 16): v-pass half warps crossing planes stay conflict free.
+    static constexpr int VP = (HX + 1) / 4 * 4 + 2;
+    static constexpr int PV = kK2TY * VP + ((HX - kK2TY * VP) % 16 + 16) % 16;
+    static constexpr int SP = 34;
     static constexpr int G0 = VT * kK2Threads / HX;
-    static constexpr int PER_G = S * NV * HX + kK2TY * VP + NST * kK2TY * SP;  // doubles per component
+    static constexpr int PER_G = S * NVB * HX + PV + NST * kK2TY * SP;  // doubles per component
     static constexpr int GFIT = (232448 - 64 - 16 * 8 * S) / (8 * PER_G);
     static constexpr int G = WS && GFIT < G0 ? GFIT : G0;  // components per group
     static constexpr int NG = (Dims<Q>::KM + G - 1) / G;
-    static constexpr int CWH = WS || G * kK2TY * (kK2TX / 8) <= kK2Threads ? 8 : 16;  // h-pass outputs per task
+#ifndef FLR_K2_WS_CWH
+#define FLR_K2_WS_CWH 8
+#endif
+    static constexpr int CWH = WS ? FLR_K2_WS_CWH : G * kK2TY * (kK2TX / 8) <= kK2Threads ? 8 : 16;  // h-pass outputs per task
     static constexpr int NCH = kK2TX / CWH;     // h-pass chunks per row
-    static constexpr size_t BOXD = (size_t)G * NV * HX;    // doubles per TMA box
+    static constexpr size_t BOXD = (size_t)G * NVB * HX;   // doubles per TMA box
     static constexpr size_t BOX = (BOXD + 15) / 16 * 16;  // stage pitch: TMA needs 128-byte aligned smem
-    static constexpr size_t VB = (size_t)G * kK2TY * VP;
+    static constexpr size_t VB = (size_t)G * PV;
     static constexpr size_t ST = (size_t)G * kK2TY * SP;
-    static constexpr size_t MODB = (size_t)kK2Threads * Dims<Q>::MSTRIDE * sizeof(float);
+    static constexpr int MSP = k2_msp<Q>;
+    static constexpr size_t MODB = (size_t)kK2Threads * MSP * sizeof(float);
     static constexpr size_t RING = S * BOX;  // doubles
     static constexpr size_t DATA = (RING + VB + NST * ST) * sizeof(double);
     // k2_tile stages the models over everything; the warp-specialised kernel in the ring
@@ -84,15 +102,16 @@ using K2WsGeom = K2Geom<Q, R, true>;
 template <class KG, int R, int NT>
 __device__ __forceinline__ void k2_vpass(const double* __restrict__ box, double* __restrict__ vb, const Taps& t, int i0)
 {
-    constexpr int G = KG::G, HX = KG::HX, NV = KG::NV, TY = kK2TY, VP = KG::VP, NQ = (G * HX + NT - 1) / NT;
+    constexpr int G = KG::G, HX = KG::HX, NV = KG::NV, NVB = KG::NVB, TY = kK2TY, VP = KG::VP, PV = KG::PV;
+    constexpr int NQ = (G * HX + NT - 1) / NT;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {  // one column task at a time (keeps the live set to NV values)
         const int task = i0 + q * NT, gv = task / HX, u = task - gv * HX;
         if (gv < G) {
             double v[NV];
 #pragma unroll
-            for (int i = 0; i < NV; ++i) v[i] = box[(gv * NV + i) * HX + u];
-            double* o = vb + gv * TY * VP + u + 2 * (u / 8);
+            for (int i = 0; i < NV; ++i) v[i] = box[(gv * NVB + i) * HX + u];
+            double* o = vb + gv * PV + u;
 #pragma unroll
             for (int r = 0; r < TY; ++r) {
                 double a = t.g[R] * v[r + R];
@@ -109,23 +128,22 @@ __device__ __forceinline__ void k2_vpass(const double* __restrict__ box, double*
 template <class KG, int R, int NT>
 __device__ __forceinline__ void k2_hpass(const double* __restrict__ vb, double* __restrict__ st, const Taps& t, int i0)
 {
-    constexpr int G = KG::G, RE = KG::RE, TY = kK2TY, VP = KG::VP, SP = KG::SP, NCH = KG::NCH;
+    constexpr int G = KG::G, RE = KG::RE, TY = kK2TY, VP = KG::VP, PV = KG::PV, SP = KG::SP, NCH = KG::NCH;
     constexpr int CW = KG::CWH, NW = CW + 2 * RE, NTASK = G * TY * NCH, NQ = (NTASK + NT - 1) / NT;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const int task = i0 + q * NT;
         if (task < NTASK) {
-            const int c = task % NCH, r = (task / NCH) % TY, g = task / (NCH * TY);
-            // u = CW c + i lives at CW c + i + 2 ((CW c + i) / 8) = (CW + CW / 4) c + i + 2 (i / 8)
-            const double* h = vb + (g * TY + r) * VP + c * (CW + CW / 4);
+            const int r = task % TY, c = (task / TY) % NCH, g = task / (NCH * TY);  // rows fastest
+            const double* h = vb + g * PV + r * VP + c * CW;
             double w[NW];
 #pragma unroll
             for (int i = 0; i < NW; i += 2) {
-                const double2 qq = *reinterpret_cast<const double2*>(h + i + 2 * (i / 8));
+                const double2 qq = *reinterpret_cast<const double2*>(h + i);
                 w[i] = qq.x;
                 w[i + 1] = qq.y;
             }
-            double* o = st + (g * TY + r) * SP + c * (CW + CW / 4);
+            double* o = st + (g * TY + r) * SP + c * CW;
 #pragma unroll
             for (int e = 0; e < CW; e += 2) {
                 double x0 = t.g[R] * w[e + RE], x1 = t.g[R] * w[e + 1 + RE];
@@ -134,7 +152,7 @@ __device__ __forceinline__ void k2_hpass(const double* __restrict__ vb, double* 
                     x0 = fma(t.g[R + d], w[e + RE - d] + w[e + RE + d], x0);
                     x1 = fma(t.g[R + d], w[e + 1 + RE - d] + w[e + 1 + RE + d], x1);
                 }
-                *reinterpret_cast<double2*>(o + e + 2 * (e / 8)) = make_double2(x0, x1);
+                *reinterpret_cast<double2*>(o + e) = make_double2(x0, x1);
             }
         }
     }
@@ -147,31 +165,32 @@ __device__ __forceinline__ void k2_gather(const double* __restrict__ st, double 
 #pragma unroll
     for (int g = 0; g < KG::G; ++g) {
         const int k = GRP * KG::G + g;
-        if (k < Dims<Q>::KM) blur[k] = st[(g * kK2TY + ty) * KG::SP + tx + 2 * (tx / 8)];
+        if (k < Dims<Q>::KM) blur[k] = st[(g * kK2TY + ty) * KG::SP + tx];
     }
 }
 
-// the tile's models (staged in shared memory, MSTRIDE floats per block) -> global, by the
+// the tile's models (staged in shared memory, k2_msp floats per block) -> global, by the
 // kK2Threads threads tid of the tile
 template <int Q>
 __device__ __forceinline__ void k2_store_models(const float* mstage, float* __restrict__ models, int mstride, int f,
                                                 int bx0, int by0, int Bx, int By, int tid)
 {
-    constexpr int TX = kK2TX, TY = kK2TY, MS = Dims<Q>::MSTRIDE;
+    constexpr int TX = kK2TX, TY = kK2TY, MS = Dims<Q>::MSTRIDE, MSP = k2_msp<Q>;
     const int nbx = min(TX, Bx - bx0), nrow = min(TY, By - by0);
     static_assert(MS % 4 == 0, "padded models are whole float4s");
     if (mstride == MS && (reinterpret_cast<uintptr_t>(models) & 15) == 0) {  // rows: contiguous aligned runs
         const int q = nbx * (MS / 4);
         for (int i = tid; i < nrow * q; i += kK2Threads) {
-            const int r = i / q, j = i - r * q;
+            const int r = i / q, j = i - r * q, b = 4 * j / MS;  // float4 j lies in block b
+            const float* m = mstage + (r * TX + b) * MSP + 4 * j - b * MS;
             reinterpret_cast<float4*>(models + ((size_t)(f * By + by0 + r) * Bx + bx0) * MS)[j] =
-                reinterpret_cast<const float4*>(mstage + r * TX * MS)[j];
+                make_float4(m[0], m[1], m[2], m[3]);
         }
     } else {  // the ABI's packed [Q+1][3] models (flr_fit): runs of nbx * mstride floats, 4-byte aligned
         const int q = nbx * mstride;
         for (int i = tid; i < nrow * q; i += kK2Threads) {
             const int r = i / q, j = i - r * q, b = j / mstride;
-            models[((size_t)(f * By + by0 + r) * Bx + bx0) * mstride + j] = mstage[(r * TX + b) * MS + j - b * mstride];
+            models[((size_t)(f * By + by0 + r) * Bx + bx0) * mstride + j] = mstage[(r * TX + b) * MSP + j - b * mstride];
         }
     }
     (void)TY;
@@ -223,16 +242,17 @@ __device__ __forceinline__ void k2_tile(const CUtensorMap* tmp, int f, int bx0, 
     float* mstage = reinterpret_cast<float*>(smk);
     const int bx = bx0 + tx, by = by0 + ty;
     if (bx < Bx && by < By) {
-        solve_block<Q>([&](int k) { return blur[k]; }, eps_add, eps_mul, mstage + tid * MS);
+        solve_block<Q>([&](int k) { return blur[k]; }, eps_add, eps_mul, mstage + tid * KG::MSP);
 #pragma unroll
-        for (int i = 3 * (Q + 1); i < MS; ++i) mstage[tid * MS + i] = 0.0f;
+        for (int i = 3 * (Q + 1); i < MS; ++i) mstage[tid * KG::MSP + i] = 0.0f;
     }
     __syncthreads();
     k2_store_models<Q>(mstage, models, mstride, f, bx0, by0, Bx, By, tid);
 }
 
 // the SOLVE warps' side of k_blur_solve_tile: gather each group as the blur warps publish
-// it (st_full), release the stage (st_empty), factor after group KF, finish after the last.
+// it (st_full), release the stage (st_empty), factor as the components arrive (DirectSolve:
+// row by row; TikhonovSolve: after group KF), finish after the last.
 // MODE 0: DirectSolve, 1: TikhonovSolve (raw models; the centred layout takes the row
 // kernels), 2: gather everything, then solve_block (the FLR_SOLVE_NORMALISED build).
 template <int Q, int R, int MODE>
@@ -257,15 +277,29 @@ __device__ __forceinline__ void k2_solve_role(const double* st, uint64_t* sfull,
 #endif
         k2_gather<Q, KG, grp>(st + (grp % NST) * KG::ST, blur, tx, ty);
         mbar_arrive(&sempty[grp % NST]);
-        if constexpr (grp == WG::KF && MODE != 2) {
+        if constexpr (MODE == 0) {  // factor row by row as the rows of S arrive, then the
+                                    // forward substitution as the cross moments arrive
+            using Dm = Dims<Q>;
+            constexpr int G = KG::G, BEGIN = (Dm::C_S - 1) / G;  // n and u are in
+            constexpr int RHS = cmax(Dm::s_idx(Q - 1, Q - 1) / G, (Dm::C_Y + 2) / G);  // S and Y are in
             if (active) {
-                if constexpr (MODE == 1) sv.factor(m, eps_add);
-                else sv.factor(m, eps_add, eps_mul);
+                if constexpr (grp == BEGIN) sv.begin(m);
+                static_for<Q>([&](auto K) {
+                    constexpr int k = decltype(K)::value;
+                    if constexpr (cmax(Dm::s_idx(k, Q - 1) / G, BEGIN) == grp) sv.template row<k>(m, eps_add, eps_mul);
+                });
+                if constexpr (grp == RHS) sv.rhs_begin(m);
+                static_for<Q>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    if constexpr (cmax((Dm::C_XY + 3 * i + 2) / G, RHS) == grp) sv.template fwd<i>(m);
+                });
             }
+        } else if constexpr (MODE == 1 && grp == WG::KF) {
+            if (active) sv.factor(m, eps_add);
         }
     });
     if (active) {
-        if constexpr (MODE == 0) sv.finish(m, out);
+        if constexpr (MODE == 0) sv.back_out(out);
         else if constexpr (MODE == 1) sv.finish(m, out, false);
         else solve_block<Q>(m, eps_add, eps_mul, out);
 #pragma unroll
@@ -343,7 +377,7 @@ __global__ void __launch_bounds__(kK2WsThreads, 1)
     // the models stage in the TMA ring: free once the last group has been published (its
     // v-pass, which read the last ring slot, precedes its h-pass)
     float* mstage = reinterpret_cast<float*>(smk);
-    float* out = mstage + tid * Dm::MSTRIDE;
+    float* out = mstage + tid * KG::MSP;
 #ifdef FLR_SOLVE_NORMALISED
     k2_solve_role<Q, R, 2>(st, sfull, sempty, active, out, eps_add, eps_mul, tx, ty);
 #else

@@ -257,73 +257,83 @@ __device__ __forceinline__ void solve_block_tikhonov(MomentFn&& m, double eps, O
     t.finish(m, out, centered);
 }
 
-// In two phases like TikhonovSolve: factor() reads [0, C_XY), finish() the cross moments.
+// In two phases like TikhonovSolve: factor() reads n, u and S, finish() Y and the cross moments.
 template <int Q>
 struct DirectSolve {
     using Dm = Dims<Q>;
-    double inv_n, mu[Q], M[Dm::NS], rinv[Q], muY[3];
+    double inv_n, mu[Q], M[Dm::NS], rinv[Q];
+    // begin() reads n and u; row<K>() then assembles row K of M (S row K) and computes row K
+    // of its Cholesky factor M = R^T R (R upper, in place), so a caller receiving S row by
+    // row (flr_k2.cuh) factors as it goes; factor() = begin + every row.
     template <class MomentFn>
-    __device__ __forceinline__ void factor(MomentFn&& m, double eps_add, double eps_mul)
+    __device__ __forceinline__ void begin(MomentFn&& m)
     {
         inv_n = 1.0 / m(Dm::C_N);
 #pragma unroll
         for (int j = 0; j < Q; ++j) mu[j] = m(Dm::C_U + j) * inv_n;
+    }
+    template <int K, class MomentFn>
+    __device__ __forceinline__ void row(MomentFn&& m, double eps_add, double eps_mul)
+    {
         const double om = 1.0 - eps_mul;
 #pragma unroll
-        for (int i = 0; i < Q; ++i)
-#pragma unroll
-            for (int j = i; j < Q; ++j) {
-                double w = fma(m(Dm::s_idx(i, j)), inv_n, -om * mu[i] * mu[j]);
-                if (i == j) {
-                    w += fma(eps_mul * mu[i], mu[i], eps_add);          // W^_ii
-                    w = fma(eps_add, fmax(w, 1e-300), w);                // + eps sigma^_i^2
-                }
-                M[Dm::s_idx(i, j) - Dm::C_S] = w;
+        for (int j = K; j < Q; ++j) {
+            double w = fma(m(Dm::s_idx(K, j)), inv_n, -om * mu[K] * mu[j]);
+            if (j == K) {
+                w += fma(eps_mul * mu[K], mu[K], eps_add);          // W^_ii
+                w = fma(eps_add, fmax(w, 1e-300), w);                // + eps sigma^_i^2
             }
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) muY[cc] = m(Dm::C_Y + cc) * inv_n;
-        // Cholesky M = R^T R (R upper, in place)
-        static_for<Q>([&](auto K) {
-            constexpr int k = decltype(K)::value;
-            double dkk = M[Dm::s_idx(k, k) - Dm::C_S];
-            static_for<k>([&](auto PP) {
+            M[Dm::s_idx(K, j) - Dm::C_S] = w;
+        }
+        double dkk = M[Dm::s_idx(K, K) - Dm::C_S];
+        static_for<K>([&](auto PP) {
+            constexpr int p = decltype(PP)::value;
+            const double r = M[Dm::s_idx(p, K) - Dm::C_S];
+            dkk = fma(-r, r, dkk);
+        });
+        rinv[K] = rsqrt(dkk);
+        static_for<Q - K - 1>([&](auto JJ) {
+            constexpr int j = K + 1 + decltype(JJ)::value;
+            double v = M[Dm::s_idx(K, j) - Dm::C_S];
+            static_for<K>([&](auto PP) {
                 constexpr int p = decltype(PP)::value;
-                const double r = M[Dm::s_idx(p, k) - Dm::C_S];
-                dkk = fma(-r, r, dkk);
+                v = fma(-M[Dm::s_idx(p, K) - Dm::C_S], M[Dm::s_idx(p, j) - Dm::C_S], v);
             });
-            rinv[k] = rsqrt(dkk);
-            static_for<Q - k - 1>([&](auto JJ) {
-                constexpr int j = k + 1 + decltype(JJ)::value;
-                double v = M[Dm::s_idx(k, j) - Dm::C_S];
-                static_for<k>([&](auto PP) {
-                    constexpr int p = decltype(PP)::value;
-                    v = fma(-M[Dm::s_idx(p, k) - Dm::C_S], M[Dm::s_idx(p, j) - Dm::C_S], v);
-                });
-                M[Dm::s_idx(k, j) - Dm::C_S] = v * rinv[k];
-            });
+            M[Dm::s_idx(K, j) - Dm::C_S] = v * rinv[K];
         });
     }
-    template <class MomentFn, class OutT>
-    __device__ __forceinline__ void finish(MomentFn&& m, OutT&& out)
+    template <class MomentFn>
+    __device__ __forceinline__ void factor(MomentFn&& m, double eps_add, double eps_mul)
     {
-        double c[Q][3];
+        begin(m);
+        static_for<Q>([&](auto K) { row<decltype(K)::value>(m, eps_add, eps_mul); });
+    }
+    // The right-hand sides, also incrementally: rhs_begin() reads Y; fwd<I>() forms the
+    // cross covariances of guide I and runs row I of the forward substitution R^T z = c
+    // (needs Cholesky rows 0..I); back_out() the back substitution R a = z and the raw model.
+    double muY[3], c[Q][3];
+    template <class MomentFn>
+    __device__ __forceinline__ void rhs_begin(MomentFn&& m)
+    {
 #pragma unroll
-        for (int i = 0; i < Q; ++i)
+        for (int cc = 0; cc < 3; ++cc) muY[cc] = m(Dm::C_Y + cc) * inv_n;
+    }
+    template <int I, class MomentFn>
+    __device__ __forceinline__ void fwd(MomentFn&& m)
+    {
 #pragma unroll
-            for (int cc = 0; cc < 3; ++cc) c[i][cc] = fma(m(Dm::C_XY + i * 3 + cc), inv_n, -mu[i] * muY[cc]);
-        // R^T z = c, R a = z (3 channels interleaved), raw model
-        static_for<Q>([&](auto K) {
-            constexpr int k = decltype(K)::value;
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-                double v = c[k][cc];
-                static_for<k>([&](auto PP) {
-                    constexpr int p = decltype(PP)::value;
-                    v = fma(-M[Dm::s_idx(p, k) - Dm::C_S], c[p][cc], v);
-                });
-                c[k][cc] = v * rinv[k];
-            }
-        });
+        for (int cc = 0; cc < 3; ++cc) {
+            double v = fma(m(Dm::C_XY + I * 3 + cc), inv_n, -mu[I] * muY[cc]);
+            static_for<I>([&](auto PP) {
+                constexpr int p = decltype(PP)::value;
+                v = fma(-M[Dm::s_idx(p, I) - Dm::C_S], c[p][cc], v);
+            });
+            c[I][cc] = v * rinv[I];
+        }
+    }
+    template <class OutT>
+    __device__ __forceinline__ void back_out(OutT&& out)
+    {
         static_for<Q>([&](auto KK) {
             constexpr int k = Q - 1 - decltype(KK)::value;
 #pragma unroll
@@ -346,6 +356,13 @@ struct DirectSolve {
             }
             out[cc] = (float)bias;
         }
+    }
+    template <class MomentFn, class OutT>
+    __device__ __forceinline__ void finish(MomentFn&& m, OutT&& out)
+    {
+        rhs_begin(m);
+        static_for<Q>([&](auto I) { fwd<decltype(I)::value>(m); });
+        back_out(out);
     }
 };
 

@@ -57,7 +57,7 @@ int main(int argc, char** argv)
         cudaFuncSetAttribute(k_blur_solve_tile<Q, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KG::SMEM);
         const dim3 gt(cdiv(Bx, kK2TX), cdiv(By, kK2TY), n);
         CUtensorMap tmk;
-        make_tmap_3d(&tmk, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * KM, KG::HX, KG::NV, KG::G);
+        make_tmap_3d(&tmk, mom, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, Bx, By, Bxp, n * KM, KG::HX, KG::NVB, KG::G);
         float tt = 0;
         for (int rep = 0; rep < 2000; ++rep) {
             if (rep == 1990) cudaEventRecord(e[0]);
