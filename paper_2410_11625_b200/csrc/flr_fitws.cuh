@@ -181,7 +181,12 @@ __device__ __forceinline__ void fit_ws_rows(Acc& acc, float (&cs)[Q], const floa
     using C = FitWsCfg<Q, MOD, HG>;
     constexpr int S = C::S, STG = C::STG, RB = C::RB;
     {  // the block shift c = its top-left pixel (first row of the item)
+#ifndef FLR_FITWS_NOWAIT
         mbar_wait(&full[k % S], (k / S) & 1);
+#else  // timing experiment (tools/t_rate.cu): the producer fills the ring once, the consumers
+       // re-read it -- the consumers' compute rate alone
+        if (k < S) mbar_wait(&full[k % S], (k / S) & 1);
+#endif
         const float* st = ring + (k % S) * STG;
 #pragma unroll
         for (int j = 0; j < Q; ++j)
@@ -190,7 +195,11 @@ __device__ __forceinline__ void fit_ws_rows(Acc& acc, float (&cs)[Q], const floa
 #pragma unroll 1  // keep the row body resident in the instruction cache
     for (int r0 = 0; r0 < rows; r0 += RB, ++k) {
         const int slot = k % S;
+#ifndef FLR_FITWS_NOWAIT
         mbar_wait(&full[slot], (k / S) & 1);
+#else
+        if (k < S) mbar_wait(&full[slot], (k / S) & 1);
+#endif
         const float* st = ring + slot * STG;
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
@@ -259,6 +268,21 @@ __device__ __forceinline__ void fit_consume_item_rel(const FitArgs& a, int it, i
         fit_ws_rows<Q, D, true, MOD, HG>(acc, cs, ring, full, rel, k, rows, lane, lb0, x0, a.W, a.afloor);
     else
         fit_ws_rows<Q, D, false, MOD, HG>(acc, cs, ring, full, rel, k, rows, lane, lb0, x0, a.W, a.afloor);
+#ifdef FLR_FITWS_NOEPI  // timing experiment (tools/t_rate.cu): no epilogue (accumulators kept live)
+    {
+        float z = 0.f;
+#pragma unroll
+        for (int i = 0; i < Dm::NS; ++i) z += lo2(acc.S[i]) + hi2(acc.S[i]);
+#pragma unroll
+        for (int i = 0; i < 3 * Q; ++i) z += lo2(acc.XY[i]) + hi2(acc.XY[i]);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) z += lo2(acc.U[i]) + hi2(acc.U[i]);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) z += lo2(acc.Y[i]) + hi2(acc.Y[i]);
+        if (z == 12345.f) a.mom[lane] = z;
+    }
+    return;
+#endif
     // epilogue: fold, then un-shift to fp64 and store (lanes of a block split the components)
     V u[Q], sv[Dm::NS], yc[3], xy[3 * Q];
     fold_pairs(acc.U, u, DQ);
@@ -273,7 +297,11 @@ __device__ __forceinline__ void fit_consume_item_rel(const FitArgs& a, int it, i
         const int gi = lane % DQ;
         const double nn = (double)(min(D, a.W - bx * D) * rows);
         const size_t cst = (size_t)a.By * a.Bxp;
+#ifdef FLR_FIT_MOM_ALIAS  // timing experiment (tools/t_rate.cu): every frame's moments in one L2-resident field
+        double* out = a.mom + (size_t)by * a.Bxp + bx;
+#else
         double* out = a.mom + (size_t)f * Dm::KM * cst + (size_t)by * a.Bxp + bx;
+#endif
         auto put = [&](int kk, double v) {
             if (kk % DQ == gi) out[(size_t)kk * cst] = v;
         };
@@ -362,7 +390,11 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
         const unsigned mask = __activemask();
         while (__any_sync(mask, it < nitems)) {
             const int slot = k % S;
+#ifndef FLR_FITWS_NOWAIT
             if (it < nitems && (k < S || mbar_test_wait(&empty[c * S + slot], ((k / S) - 1) & 1))) {
+#else
+            if (it < nitems && k < S) {
+#endif
                 ws_proxy_fence();
                 fit_issue_row<Q, D, MOD, HG, kFS, C::RB>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG,
                                                          &full[c * S + slot], pg, py);
@@ -373,6 +405,9 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
                     decode();
                 }
             }
+#ifdef FLR_FITWS_NOWAIT
+            if (k >= S) it = nitems;
+#endif
         }
         if (a.early && lane == 0) {  // (each trigger follows a completed wait: safe from any producer)
             pdl_wait();

@@ -17,3 +17,5 @@ for V in staged fused; do
 timeout -s KILL 600 ncu --replay-mode app-range --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum --csv --log-file gpurun_out/r02_step_traffic_$V.csv python tools/step_traffic.py $V > gpurun_out/ncu_step_$V.log 2>&1; echo "ncu step $V rc=$?"
 done
 timeout -s KILL 60 tools/t_timeline > gpurun_out/r02_timeline.txt 2>&1; head -4 gpurun_out/r02_timeline.txt
+# the blur+solve kernel alone (1080p Q=8 R=3 moment field): full capture for shared-memory wavefronts / fp64 pipe
+timeout -s KILL 300 ncu --set full --import-source on --clock-control none -k regex:k_blur_solve_tile -s 5 -c 1 -o gpurun_out/r02_k2 tools/t_k2 1 > gpurun_out/ncu_k2.log 2>&1; echo "ncu k2 rc=$?"

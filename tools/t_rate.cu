@@ -122,6 +122,7 @@ int main()
         }
         const double tf = 1e-3 * ms / reps;
         double tself = 0;
+#ifndef FLR_FITWS_NOWAIT  // (self-fed warps would exit with stages in flight)
         {
             using SC = FitSelfCfg<Q>;
             static bool once = false;
@@ -135,6 +136,7 @@ int main()
             }
             tself = 1e-3 * ms / reps;
         }
+#endif
         for (int k = 0; k < 2; ++k) {
             cudaEventRecord(e0);
             for (int r = 0; r < reps; ++r) k_apply_ws<Q><<<g, AC::THREADS, AC::SMEM>>>(aa, nf);

@@ -82,6 +82,12 @@ int main(int argc, char** argv)
         printf("%-5s ctas %3d  entry %6.2f..%6.2f  wait-passed %6.2f..%6.2f  exit %6.2f..%6.2f  mean busy %5.2f us\n",
                nm[k], ncta[k], (emin - t0) * 1e-3, (emax - t0) * 1e-3, (wmin - t0) * 1e-3, (wmax - t0) * 1e-3,
                (xmin - t0) * 1e-3, (xmax - t0) * 1e-3, dur / ncta[k] * 1e-3);
+        std::vector<double> xs;
+        for (int c = 0; c < ncta[k]; ++c) xs.push_back((tl[(k * 1024 + c) * 4 + 2] - t0) * 1e-3);
+        std::sort(xs.begin(), xs.end());
+        printf("      exit deciles:");
+        for (int d = 0; d <= 10; ++d) printf(" %.1f", xs[std::min((int)xs.size() - 1, d * (int)xs.size() / 10)]);
+        printf("\n");
     }
     if (argc > 1 && std::string(argv[1]) == "cta") {  // fit: per-CTA exit (relative), SM id, items
         std::vector<std::pair<long long, int>> ex;

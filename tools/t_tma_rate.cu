@@ -7,6 +7,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include "../paper_2410_11625_b200/csrc/flr_pipe.cuh"
 using namespace flr;
 
@@ -119,7 +121,18 @@ __global__ void __launch_bounds__(512, 1) k_ws(const __grid_constant__ Args a, i
         const int slot = k % S;
         mbar_wait(&full[w * S + slot], (k / S) & 1);
         acc += reinterpret_cast<float*>(sm)[(size_t)(w * S + slot) * stg_floats + lane];
-        for (int i = 0; i < spin; ++i) acc = fmaf(acc, 1.0001f, 0.5f);
+        if (spin > 0) {
+            for (int i = 0; i < spin; ++i) acc = fmaf(acc, 1.0001f, 0.5f);
+        } else if (spin < 0) {  // issue-heavy hold: -spin rounds of 32 independent FFMA2 (the fit's mix)
+            f2 h[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) h[j] = pk2(acc + j, acc - j);
+            for (int i = 0; i < -spin; ++i)
+#pragma unroll
+                for (int j = 0; j < 32; ++j) h[j] = fma2(h[j], h[(j + 1) & 31], h[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc += lo2(h[j]);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[w * S + slot]);
     }
@@ -148,10 +161,14 @@ int main()
                         {128, 1, 16, 2, 8, 8}, {128, 1, 12, 3, 8, 8}, {256, 1, 8, 2, 8, 8}, {128, 2, 8, 2, 4, 8},
                         {64, 1, 16, 4, 8, 8}, {128, 1, 4, 8, 8, 8}};
     cudaFuncSetAttribute(k_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    const bool spins = getenv("TMA_SPINS") != nullptr;  // the fit's protocol with a per-stage hold time
     for (int G : {37, 148}) {
         struct WC { int NC, S, rb; };
-        for (int spin : {0}) {
-            for (WC wc : {WC{7, 4, 1}, WC{7, 2, 2}, WC{6, 3, 2}, WC{7, 1, 4}, WC{3, 2, 4}, WC{5, 2, 2}}) {
+        const std::vector<int> spin_list = spins ? std::vector<int>{0, 400, -4, -6, -8, -10} : std::vector<int>{0};
+        const std::vector<WC> wc_list = spins ? std::vector<WC>{WC{7, 2, 2}}
+                                              : std::vector<WC>{WC{7, 4, 1}, WC{7, 2, 2}, WC{6, 3, 2}, WC{7, 1, 4}, WC{3, 2, 4}, WC{5, 2, 2}};
+        for (int spin : spin_list) {
+            for (WC wc : wc_list) {
             const int NC = wc.NC, S = wc.S;
             Args a;
             a.W = W, a.H = H, a.P = P, a.nf = NF, a.bx = 128, a.by = wc.rb, a.rpi = 8 / wc.rb, a.split = 8;
@@ -178,6 +195,7 @@ int main()
                    bytes / ms / 1e6, bytes / ms / 1e6 / G, cudaGetErrorString(cudaGetLastError()));
             }
         }
+        if (spins) continue;
         for (const Cfg& c : cfgs) {
             Args a;
             a.W = W, a.H = H, a.P = P, a.nf = NF, a.bx = c.bx, a.by = c.by, a.rpi = c.rpi, a.split = c.split;
