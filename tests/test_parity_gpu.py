@@ -118,6 +118,18 @@ def test_odd_sizes_every_block(flr, oracle_mod, W, H, block):
     assert_parity(out, ref, f"{W}x{H} block={block}")
 
 
+@pytest.mark.parametrize("Q", [1, 3, 5, 8])
+@pytest.mark.parametrize("radius", [1, 2, 4, 6, 7])
+def test_k2_tile_geometries(flr, oracle_mod, Q, radius):
+    """The warp-specialised K2 tile (flr_k2.cuh) for every halo geometry: R = 1, 2 (36 halo
+    columns), 4 (TMA box padded by one row), 6, 7 (3-stage ring, G = 5-6 components per group),
+    ragged tiles in x and y (Bx = 38, By = 25 at block 8)."""
+    G, Y = _inputs(300, 200, Q, 3500 + 10 * Q + radius)
+    out, ref = _run_denoise(flr, oracle_mod, G, Y, radius=radius)
+    assert_parity(out, ref, f"Q={Q} R={radius}")
+    assert "k_blur_solve_tile" in flr.last_launch_names()
+
+
 @pytest.mark.parametrize("radius", [1, 3, 5, 8, 10])
 def test_sweep_radius(flr, oracle_mod, radius):
     G, Y = _inputs(128, 96, 8, 3300 + radius)
