@@ -24,7 +24,13 @@ namespace flr {
 #endif
 constexpr int kApplyWsNC = FLR_APPLYWS_NC;  // consumer warps (+1 producer = 8 warps, 255-register cap)
 constexpr int kApplyWsS = FLR_APPLYWS_S;  // guide-row stages per consumer
-constexpr int kApplyWsM = 2;   // model stages per consumer
+#ifndef FLR_APPLYWS_M
+#define FLR_APPLYWS_M 2
+#endif
+#ifndef FLR_APPLYWS_S2
+#define FLR_APPLYWS_S2 2
+#endif
+constexpr int kApplyWsM = FLR_APPLYWS_M;   // model stages per consumer
 
 template <int Q, bool MOD = false, bool HG = false>
 struct ApplyWsCfg {
@@ -46,7 +52,8 @@ struct ApplyWsCfg {
         return (s <= 2 || (size_t)kApplyWsNC * ((s * ROWF + kApplyWsM * MODF + 31) / 32 * 32) * 4 + 4096 <= 232448)
                    ? s : fit_stages(s - 1);
     }
-    static constexpr int NC = kApplyWsNC, S = TWO ? 2 : fit_stages(kApplyWsS), SM = kApplyWsM, THREADS = (NC + 1) * 32;
+    static constexpr int NC = kApplyWsNC, S = TWO ? fit_stages(FLR_APPLYWS_S2) : fit_stages(kApplyWsS), SM = kApplyWsM,
+                         THREADS = (NC + 1) * 32;
     static constexpr int WARPF = (S * ROWF + SM * MODF + 31) / 32 * 32;  // 128-byte aligned regions
     static constexpr size_t BAR_OFF = (size_t)NC * WARPF * sizeof(float);
     static constexpr int NBAR = 2 * (S + SM);  // full + empty per stage
@@ -92,7 +99,11 @@ __device__ __forceinline__ void apply_consume_item(const ApplyArgs& a, const App
     f2 top0[MP], dlt0[MP], top1[MP], dlt1[MP];
     {
         const int ms = km % SM;
+#ifndef FLR_APPLYWS_NOWAIT
         mbar_wait(&mfull[ms], (km / SM) & 1);
+#else  // timing experiment (tools/t_rate.cu): rings filled once and re-read -- the consumers' arithmetic alone
+        if (km < SM) mbar_wait(&mfull[ms], (km / SM) & 1);
+#endif
         const float* mod = mod_st + ms * C::MODF;
 #pragma unroll
         for (int v = 0; v < MS / 4; ++v) {
@@ -113,7 +124,11 @@ __device__ __forceinline__ void apply_consume_item(const ApplyArgs& a, const App
 #pragma unroll 1
     for (int ys = g.y0; ys < g.y1; ys += C::RB, ++kr) {
         const int rs = kr % S;
+#ifndef FLR_APPLYWS_NOWAIT
         mbar_wait(&rfull[rs], (kr / S) & 1);
+#else
+        if (kr < S) mbar_wait(&rfull[rs], (kr / S) & 1);
+#endif
         const float* st = rows_st + rs * C::ROWF;
         float o[C::RB][3][4];
 #pragma unroll
@@ -255,6 +270,9 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws
         if (lane == 0) FLR_TL(2, 1);
         constexpr unsigned mask = (1u << NC) - 1;
         while (__any_sync(mask, it < nitems)) {
+#ifdef FLR_APPLYWS_NOWAIT
+            if (kr >= S && km >= SM) it = nitems;
+#endif
             if (it >= nitems) continue;
             if (need_models) {
                 const int s = km % SM;

@@ -68,6 +68,14 @@ static int num_sms()
     return sms;
 }
 
+#ifndef FLR_APPLY_SUB_ROWS
+#define FLR_APPLY_SUB_ROWS 8
+#endif
+// fewest output rows of an APPLY item (items = sub-bands of a block row of models): whole
+// 8-row bands at D = 8 halve the per-item model copies and producer operations (C2 44.15 vs
+// 44.5 us per frame with 4-row items; the per-SM apply rate 61 vs 51 GB/s at 37 SMs)
+constexpr int kApplySubRows = FLR_APPLY_SUB_ROWS;
+
 // K1: the warp-specialised TMA kernel when the planes allow it, else the tiled kernel
 template <int Q, int D>
 static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
@@ -227,7 +235,7 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
         a.models = models, a.out = out;
         a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W, kSeg), a.nband = apply_nband(H, D, By);
         a.nsub = 1;
-        while (D % (2 * a.nsub) == 0 && D / (2 * a.nsub) >= 4)
+        while (D % (2 * a.nsub) == 0 && D / (2 * a.nsub) >= kApplySubRows)
             a.nsub *= 2;
         a.reverse = 1;
         using C = ApplyWsCfg<Q, false, true>;
@@ -257,7 +265,7 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
         a.models = models, a.out = out;
         a.W = W, a.H = H, a.D = D, a.Bx = Bx, a.By = By, a.nseg = cdiv(W, kSeg), a.nband = apply_nband(H, D, By);
         a.nsub = 1;
-        while (D % (2 * a.nsub) == 0 && D / (2 * a.nsub) >= 4)
+        while (D % (2 * a.nsub) == 0 && D / (2 * a.nsub) >= kApplySubRows)
             a.nsub *= 2;
         a.reverse = 1;
         using C = ApplyWsCfg<Q, true>;
@@ -271,8 +279,8 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
     if (D % 8 == 0 && mstride == Dims<Q>::MSTRIDE && aligned(models, 16)) {
         const int off = (D / 2) % 8;
         ApplyArgs a;
-        int nsub = 1;  // sub-bands of >= 4 rows: finer items balance the warps of one frame
-        while (D % (2 * nsub) == 0 && D / (2 * nsub) >= 4)
+        int nsub = 1;  // sub-bands of >= kApplySubRows rows (finer items balance the warps of one frame)
+        while (D % (2 * nsub) == 0 && D / (2 * nsub) >= kApplySubRows)
             nsub *= 2;
         if (vec_ok(G, W) && vec_ok(out, W) &&
             make_tmap_planes(&a.tg, G, W, H, n * Q, kSeg, Q, ApplyWsCfg<Q>::RB)) {  // TMA path

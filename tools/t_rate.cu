@@ -4,6 +4,9 @@
 // per-SM rate limit is reached; the knee gives the rate one SM can stream at.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude -lcuda tools/t_rate.cu -o tools/t_rate
 #include <cstdio>
+#ifndef T_NSUB
+#define T_NSUB 2  // APPLY sub-bands per block row (the library: 2 at D = 8)
+#endif
 #include "../paper_2410_11625_b200/csrc/flr_launch.h"
 #include "../paper_2410_11625_b200/csrc/flr_fitws.cuh"
 #include "../paper_2410_11625_b200/csrc/flr_applyws.cuh"
@@ -108,7 +111,7 @@ int main()
     ApplyArgs aa{};
     make_tmap_planes(&aa.tg, G, W, H, nf * Q, kSeg, Q, ApplyWsCfg<Q>::RB);
     aa.models = M, aa.out = O, aa.W = W, aa.H = H, aa.D = D, aa.Bx = Bx, aa.By = By;
-    aa.nseg = W / kSeg, aa.nband = apply_nband(H, D, By), aa.nsub = 2;
+    aa.nseg = W / kSeg, aa.nband = apply_nband(H, D, By), aa.nsub = T_NSUB;
     const double fit_bytes = (double)plane * (Q + 3) * 4 * nf, app_bytes = (double)plane * (Q + 3) * 4 * nf;
     for (int g : {148, 136, 120, 104, 88, 74, 60, 48, 37}) {
         float ms = 0;

@@ -38,12 +38,13 @@ int main(int argc, char** argv)
     for (int i = -3; i <= 3; ++i) t.g[3 + i] = std::exp(-(double)(i * i) / (2.0 * 1.25 * 1.25));
     cudaStream_t s;
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    const std::string mode = "staged";
+    const bool noapply = argc > 1 && std::string(argv[argc - 1]) == "noapply";  // fit + K2 only
+    const std::string mode = noapply ? "staged (no apply)" : "staged";
     auto step = [&](int k) {
         LaunchCtx ctx;
         ctx.s = s;
         launch_fit<Q>(1, W, H, D, Bx, By, G[k], Y[k], raw, mom, hb, models, Dims<Q>::MSTRIDE, 1e-5, 1e-4, t, ctx);
-        launch_apply<Q>(1, W, H, D, Bx, By, models, Dims<Q>::MSTRIDE, G[k], O[k], ctx);
+        if (!noapply) launch_apply<Q>(1, W, H, D, Bx, By, models, Dims<Q>::MSTRIDE, G[k], O[k], ctx);
     };
     for (int i = 0; i < 20; ++i) step(i % NP);
     cudaGraph_t g;
