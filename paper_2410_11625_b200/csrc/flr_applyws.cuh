@@ -3,8 +3,9 @@
 //
 // One CTA per SM: kApplyWsNC consumer warps + 1 producer warp.  Lane c of the producer
 // walks consumer c's APPLY items (sub-band of D/nsub output rows x 128 pixels) and keeps
-// two rings full: the item's 2 x 18 staged models (two 1-D bulk copies, 2 stages) and its
-// guide rows (one 3-D TMA box {128, 1, Q} per row, kApplyWsS stages).  Consumers run no
+// two rings full: the items' 2 x 18 staged models (two 1-D bulk copies per item, kApplyWsM
+// stages, running ahead of the rows: a stage is free once its models are in registers) and
+// the guide rows (one 3-D TMA box {128, RB, Q} per stage, 3 stages of 2 rows at Q = 8).  Consumers run no
 // producer code: per item each lane keeps its two model columns (top row and bottom-top
 // difference) in registers; per row it forms A_y = top + t_y (bottom - top), reads its
 // pixel quad of the Q guide planes, and applies I = (1 - t_x) x~.A_y(i0) + t_x x~.A_y(i1)
@@ -25,12 +26,15 @@ namespace flr {
 constexpr int kApplyWsNC = FLR_APPLYWS_NC;  // consumer warps (+1 producer = 8 warps, 255-register cap)
 constexpr int kApplyWsS = FLR_APPLYWS_S;  // guide-row stages per consumer
 #ifndef FLR_APPLYWS_M
-#define FLR_APPLYWS_M 2
+#define FLR_APPLYWS_M 1
 #endif
 #ifndef FLR_APPLYWS_S2
-#define FLR_APPLYWS_S2 2
+#define FLR_APPLYWS_S2 3
 #endif
-constexpr int kApplyWsM = FLR_APPLYWS_M;   // model stages per consumer
+#ifndef FLR_SMEM_RESERVE
+#define FLR_SMEM_RESERVE 4096  // bytes kept free for barriers and static shared memory
+#endif
+constexpr int kApplyWsM = FLR_APPLYWS_M;   // model stages per consumer (1: the smem goes to a third row stage)
 
 template <int Q, bool MOD = false, bool HG = false>
 struct ApplyWsCfg {
@@ -43,13 +47,13 @@ struct ApplyWsCfg {
     // a row stage holds RB output rows (one TMA box {128, RB, planes} per tensor): two rows
     // per box double what the producer warp can issue per SM (see FitWsCfg); RB = 2 with 2
     // stages when that fits in 227 KB, else single rows with up to kApplyWsS stages
-    static constexpr bool TWO = (size_t)kApplyWsNC * ((2 * 2 * ROW1 + kApplyWsM * MODF + 31) / 32 * 32) * 4 + 4096 <=
+    static constexpr bool TWO = (size_t)kApplyWsNC * ((2 * 2 * ROW1 + kApplyWsM * MODF + 31) / 32 * 32) * 4 + FLR_SMEM_RESERVE <=
                                 232448;
     static constexpr int RB = TWO ? 2 : 1;
     static constexpr int ROWF = RB * ROW1;  // floats per row stage
     static constexpr int fit_stages(int s)
     {
-        return (s <= 2 || (size_t)kApplyWsNC * ((s * ROWF + kApplyWsM * MODF + 31) / 32 * 32) * 4 + 4096 <= 232448)
+        return (s <= 2 || (size_t)kApplyWsNC * ((s * ROWF + kApplyWsM * MODF + 31) / 32 * 32) * 4 + FLR_SMEM_RESERVE <= 232448)
                    ? s : fit_stages(s - 1);
     }
     static constexpr int NC = kApplyWsNC, S = TWO ? fit_stages(FLR_APPLYWS_S2) : fit_stages(kApplyWsS), SM = kApplyWsM,
@@ -245,51 +249,52 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws
         uint64_t* mfull = rempty + S;
         uint64_t* mempty = mfull + SM;
         const uint64_t pg = policy_evict_first(), pm = policy_evict_normal();
-        int it = blockIdx.x * NC + c, f = 0, y = 0, kr = 0, km = 0, pre = 0;
-        ApplyGeom g;
-        bool need_models = true;
-        auto next_item = [&]() {  // skip empty sub-bands (rows outside the image)
-            for (; it < nitems; it += GW) {
-                g = geom(it, f);
-                if (g.y0 < g.y1) break;
+        // two cursors over the consumer's items: the guide rows (it, y) and the models (itm),
+        // which run up to SM items ahead -- a model stage is free as soon as the consumer has
+        // its models in registers, so the next item's models are in flight while this one's
+        // rows stream (models issued only once the rows of an item were queued left every
+        // item start waiting one L2 round trip for its models)
+        int it = blockIdx.x * NC + c, itm, f = 0, fm = 0, y = 0, kr = 0, km = 0;
+        ApplyGeom g, gm;
+        auto valid = [&](int& i, ApplyGeom& gg, int& ff) {  // skip empty sub-bands (rows outside the image)
+            for (; i < nitems; i += GW) {
+                gg = geom(i, ff);
+                if (gg.y0 < gg.y1) break;
             }
-            y = g.y0;
-            need_models = true;
         };
-        next_item();
-        {  // guide rows of the first item, ahead of the models (and of the wait)
-            int pit = it, py0 = y;
-            for (; kr < S && pit < nitems && py0 < g.y1; ++kr, py0 += C::RB) {
-                ws_proxy_fence();
-                apply_issue_row<Q, MOD, HG, C::RB>(a, g, f, py0, rows_st + kr * C::ROWF, &rfull[kr], pg);
+        valid(it, g, f);
+        y = g.y0;
+        itm = it, gm = g, fm = f;
+        // guide rows of the first item, ahead of the models (and of the wait): the guides are
+        // inputs of the call
+        for (; kr < S && it < nitems; ++kr) {
+            ws_proxy_fence();
+            apply_issue_row<Q, MOD, HG, C::RB>(a, g, f, y, rows_st + kr * C::ROWF, &rfull[kr], pg);
+            if ((y += C::RB) >= g.y1) {
+                it += GW;
+                valid(it, g, f);
+                y = g.y0;
             }
-            pre = kr;
         }
         pdl_wait();  // the models come from the previous grid
         if (lane == 0) pdl_trigger();
         if (lane == 0) FLR_TL(2, 1);
         constexpr unsigned mask = (1u << NC) - 1;
-        while (__any_sync(mask, it < nitems)) {
+        while (__any_sync(mask, it < nitems || itm < nitems)) {
 #ifdef FLR_APPLYWS_NOWAIT
-            if (kr >= S && km >= SM) it = nitems;
+            if (kr >= S && km >= SM) it = itm = nitems;
 #endif
-            if (it >= nitems) continue;
-            if (need_models) {
+            if (itm < nitems) {
                 const int s = km % SM;
                 if (km < SM || mbar_test_wait(&mempty[s], ((km / SM) - 1) & 1)) {
                     ws_proxy_fence();
-                    apply_issue_models<Q>(a, g, f, mod_st + s * C::MODF, &mfull[s], pm);
+                    apply_issue_models<Q>(a, gm, fm, mod_st + s * C::MODF, &mfull[s], pm);
                     ++km;
-                    need_models = false;
+                    itm += GW;
+                    valid(itm, gm, fm);
                 }
-            } else if (pre > 0) {  // rows of the first item already queued before the wait
-                y += pre * C::RB;
-                pre = 0;
-                if (y >= g.y1) {
-                    it += GW;
-                    next_item();
-                }
-            } else {
+            }
+            if (it < nitems) {
                 const int s = kr % S;
                 if (kr < S || mbar_test_wait(&rempty[s], ((kr / S) - 1) & 1)) {
                     ws_proxy_fence();
@@ -297,7 +302,8 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws
                     ++kr;
                     if ((y += C::RB) >= g.y1) {
                         it += GW;
-                        next_item();
+                        valid(it, g, f);
+                        y = g.y0;
                     }
                 }
             }
