@@ -480,3 +480,49 @@ def test_p14_tikhonov_huge_eps_shrinks_to_zero(oracle_mod):
     G, Y = _scene(rng)
     out = oracle_mod.denoise_tikhonov(G, Y, D=4, sigma=8.0, R=2, eps=1e9)
     assert np.abs(out).max() < 1e-7 * np.abs(Y).max() + 1e-12
+
+
+# ---------------------------------------------------------------- R3: the recorded divergence from SPEC
+def _clamp_pixel_weights(W, H, D, bx, by, s, R):
+    """SPEC's clamp-to-edge blur of the moment field, written on pixels:
+    window block b + d is replaced by the nearest in-grid block, so a border block's
+    moments are counted once per clamped offset (weight g(dy) g(dx) each time)."""
+    Bx, By = -(-W // D), -(-H // D)
+    wb = np.zeros((By, Bx))
+    for dy in range(-R, R + 1):
+        for dx in range(-R, R + 1):
+            wb[min(max(by + dy, 0), By - 1), min(max(bx + dx, 0), Bx - 1)] += brute.gauss(dy, s) * brute.gauss(dx, s)
+    return np.kron(wb, np.ones((D, D)))[:H, :W]
+
+
+def test_r3_clamp_to_edge_differs_only_within_r_blocks_of_the_border(oracle_mod):
+    """R3: the oracle and the kernels truncate the blur window at the
+    frame edge (zero padding); SPEC's program clamps instead.  Brute-force WLS with the
+    clamped weights gives the SAME models for every block at least R blocks from each
+    border (its window never leaves the grid) and different ones within R blocks of it;
+    the output differences it causes stay within about R + 1 blocks of the border and are
+    far above the parity bar there (so the choice is visible, and recorded, not a rounding
+    matter)."""
+    rng = np.random.default_rng(33)
+    Q, D, R, sigma = 3, 4, 2, 6.0
+    Bx, By = 9, 8
+    W, H = Bx * D, By * D
+    G = rand_planes(rng, Q, H, W, 0.1, 0.9)
+    Y = rand_planes(rng, 3, H, W, 0.0, 1.0) + 0.5 * G[:1]
+    s = sigma / D
+    A = oracle_mod.fit(G, Y, D=D, sigma=sigma, R=R)[0]
+    Ac = np.zeros_like(A)
+    for by in range(By):
+        for bx in range(Bx):
+            Ac[by, bx] = brute.ridge_lstsq_model(G, Y, _clamp_pixel_weights(W, H, D, bx, by, s, R), 1e-5, 1e-4)
+    inner = np.zeros((By, Bx), bool)
+    inner[R:By - R, R:Bx - R] = True
+    diff = np.abs(A - Ac).max(axis=(2, 3))
+    assert diff[inner].max() < 1e-8, diff[inner].max()
+    assert diff[~inner].min() > 1e-6, diff[~inner].min()
+    O = oracle_mod.apply(A[None], G[None], D)[0]
+    Oc = brute.apply_blend(Ac, G, D)
+    od = np.abs(O - Oc).max(axis=0)
+    m = (R + 1) * D  # pixels whose four blended models are all inner blocks
+    assert od[m:H - m, m:W - m].max() < 1e-8
+    assert od.max() > 1e-3  # ~100x the 1e-5 absolute parity bar
