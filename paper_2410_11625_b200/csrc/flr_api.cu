@@ -348,6 +348,9 @@ flr_status denoise_upsample_impl(int32_t n, int32_t Q, int32_t W_lo, int32_t H_l
     if (hg && (!half_guides_fit_ok(D, W_lo, guides_lo, radiance_lo) ||
                !half_guides_apply_ok(Dout, W_hi, models, guides_hi, out)))
         return FLR_ERR_UNSUPPORTED;
+    // denoise (U = 1, one guide set): the apply re-reads the fit's guides, which the fit then
+    // leaves in L2 when they fit there (launch_fit)
+    ctx.keep_guides = !hg && guides_lo == guides_hi;
     if ((st = do_fit(n, Q, W_lo, H_lo, guides_lo, radiance_lo, p, models, ms, workspace, ctx, hg)))
         return st;
     FLR_DISPATCH_Q(Q, (launch_apply<QQ>(n, W_hi, H_hi, Dout, Bx, By, models, ms, guides_hi, out, ctx, nullptr,

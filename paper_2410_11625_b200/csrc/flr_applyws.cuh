@@ -5,7 +5,7 @@
 // walks consumer c's APPLY items (sub-band of D/nsub output rows x 128 pixels) and keeps
 // two rings full: the items' 2 x 18 staged models (two 1-D bulk copies per item, kApplyWsM
 // stages, running ahead of the rows: a stage is free once its models are in registers) and
-// the guide rows (one 3-D TMA box {128, RB, Q} per stage, 3 stages of 2 rows at Q = 8).  Consumers run no
+// the guide rows (one 3-D TMA box {128, RB, Q} per stage; 2 or 3 stages of 2 rows at Q = 8).  Consumers run no
 // producer code: per item each lane keeps its two model columns (top row and bottom-top
 // difference) in registers; per row it forms A_y = top + t_y (bottom - top), reads its
 // pixel quad of the Q guide planes, and applies I = (1 - t_x) x~.A_y(i0) + t_x x~.A_y(i1)
@@ -26,17 +26,21 @@ namespace flr {
 constexpr int kApplyWsNC = FLR_APPLYWS_NC;  // consumer warps (+1 producer = 8 warps, 255-register cap)
 constexpr int kApplyWsS = FLR_APPLYWS_S;  // guide-row stages per consumer
 #ifndef FLR_APPLYWS_M
-#define FLR_APPLYWS_M 1
+#define FLR_APPLYWS_M 2
 #endif
 #ifndef FLR_APPLYWS_S2
-#define FLR_APPLYWS_S2 3
+#define FLR_APPLYWS_S2 2
 #endif
 #ifndef FLR_SMEM_RESERVE
 #define FLR_SMEM_RESERVE 4096  // bytes kept free for barriers and static shared memory
 #endif
-constexpr int kApplyWsM = FLR_APPLYWS_M;   // model stages per consumer (1: the smem goes to a third row stage)
+constexpr int kApplyWsM = FLR_APPLYWS_M;   // model stages per consumer
 
-template <int Q, bool MOD = false, bool HG = false>
+// DEEP: one model stage and three 2-row guide stages per consumer (the guides are mostly L2
+// hits -- the fit of the same call left them there: C2 43.0 vs 43.5 us per frame); the
+// default (two model stages, two guide stages) is faster when the guides stream from HBM
+// (C4 37.1 vs 37.75, 32-frame calls 43.3 vs 44.4 us per frame)
+template <int Q, bool MOD = false, bool HG = false, bool DEEP = false>
 struct ApplyWsCfg {
     using SD = StreamDims<Q>;
     // floats per output row: Q guide planes (fp32, or fp16 when HG) (+ 3 albedo and 3
@@ -44,19 +48,20 @@ struct ApplyWsCfg {
     static constexpr int GF = HG ? kSeg / 2 : kSeg;  // floats per guide plane row
     static constexpr int ROW1 = Q * GF + (MOD ? 6 : 0) * kSeg;
     static constexpr int MODF = 2 * kApplyNCol * SD::MS;  // floats per model stage
+    static constexpr int MSTG = DEEP ? 1 : kApplyWsM;     // model stages
     // a row stage holds RB output rows (one TMA box {128, RB, planes} per tensor): two rows
     // per box double what the producer warp can issue per SM (see FitWsCfg); RB = 2 with 2
     // stages when that fits in 227 KB, else single rows with up to kApplyWsS stages
-    static constexpr bool TWO = (size_t)kApplyWsNC * ((2 * 2 * ROW1 + kApplyWsM * MODF + 31) / 32 * 32) * 4 + FLR_SMEM_RESERVE <=
+    static constexpr bool TWO = (size_t)kApplyWsNC * ((2 * 2 * ROW1 + MSTG * MODF + 31) / 32 * 32) * 4 + FLR_SMEM_RESERVE <=
                                 232448;
     static constexpr int RB = TWO ? 2 : 1;
     static constexpr int ROWF = RB * ROW1;  // floats per row stage
     static constexpr int fit_stages(int s)
     {
-        return (s <= 2 || (size_t)kApplyWsNC * ((s * ROWF + kApplyWsM * MODF + 31) / 32 * 32) * 4 + FLR_SMEM_RESERVE <= 232448)
+        return (s <= 2 || (size_t)kApplyWsNC * ((s * ROWF + MSTG * MODF + 31) / 32 * 32) * 4 + FLR_SMEM_RESERVE <= 232448)
                    ? s : fit_stages(s - 1);
     }
-    static constexpr int NC = kApplyWsNC, S = TWO ? fit_stages(FLR_APPLYWS_S2) : fit_stages(kApplyWsS), SM = kApplyWsM,
+    static constexpr int NC = kApplyWsNC, S = TWO ? fit_stages(DEEP ? 3 : FLR_APPLYWS_S2) : fit_stages(kApplyWsS), SM = MSTG,
                          THREADS = (NC + 1) * 32;
     static constexpr int WARPF = (S * ROWF + SM * MODF + 31) / 32 * 32;  // 128-byte aligned regions
     static constexpr size_t BAR_OFF = (size_t)NC * WARPF * sizeof(float);
@@ -206,10 +211,10 @@ __device__ __forceinline__ void apply_consume_item(const ApplyArgs& a, const App
     }
 }
 
-template <int Q, bool MOD = false, bool HG = false>
-__global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG>::THREADS, 1) k_apply_ws(const __grid_constant__ ApplyArgs a, int n)
+template <int Q, bool MOD = false, bool HG = false, bool DEEP = false>
+__global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG, DEEP>::THREADS, 1) k_apply_ws(const __grid_constant__ ApplyArgs a, int n)
 {
-    using C = ApplyWsCfg<Q, MOD, HG>;
+    using C = ApplyWsCfg<Q, MOD, HG, DEEP>;
     if (threadIdx.x == 0) FLR_TL(2, 0);
     constexpr int NC = C::NC, S = C::S, SM = C::SM;
     extern __shared__ __align__(1024) unsigned char smem_raw[];

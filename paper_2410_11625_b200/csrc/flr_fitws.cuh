@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
         constexpr int NP = C::NP, LANES = (NC + NP - 1) / NP;
         const int p = warp - NC, c = p + NP * lane;
         if (lane >= LANES || c >= NC) return;
-        const uint64_t pg = policy_evict_first(), py = policy_evict_first();
+                const uint64_t pg = policy_by_code(a.gpol), py = policy_evict_first();
         int it = blockIdx.x * NC + c, row = 0, rows = 0, f = 0, by = 0, sg = 0;
         auto decode = [&]() {
             if (it >= nitems) return;

@@ -75,11 +75,13 @@ static int num_sms()
 // 8-row bands at D = 8 halve the per-item model copies and producer operations (C2 44.15 vs
 // 44.5 us per frame with 4-row items; the per-SM apply rate 61 vs 51 GB/s at 37 SMs)
 constexpr int kApplySubRows = FLR_APPLY_SUB_ROWS;
+// largest guide volume of one call the fit leaves in L2 (evict_normal) for the apply
+constexpr size_t kGuideL2Keep = (size_t)80 << 20;
 
 // K1: the warp-specialised TMA kernel when the planes allow it, else the tiled kernel
 template <int Q, int D>
 static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const float* Y, double* mom,
-                      cudaStream_t s, const float* A, float afloor, bool hg, bool early, bool acc64)
+                      cudaStream_t s, const float* A, float afloor, bool hg, bool early, bool acc64, bool keep)
 {
     FitArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -87,6 +89,11 @@ static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
     a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kFS);
     a.afloor = afloor;
     a.early = early;
+    // keep: the apply of this call re-reads these guides.  C2 (66 MB of guides):
+    // evict_normal guides 42.9 vs 43.55 us per frame (the apply's guide re-reads hit L2 more:
+    // -2.8 us; the fit streams next to more dirty lines: +2.2 us); lo-res (C4) and batched
+    // guides stream with evict_first
+    a.gpol = keep ? 1 : 0;
     const int items = n * By * a.nseg;
     if (hg) {  // fp16 guide planes: the warp-specialised kernel with a half-width guide stage
         using C = FitWsCfg<Q, false, true>;
@@ -140,14 +147,15 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
                 double em, const Taps& taps, LaunchCtx& ctx, const float* A, float afloor, bool hg)
 {
     const cudaStream_t s = ctx.s;
+    ctx.l2_guides = ctx.keep_guides && (size_t)n * Q * W * H * (hg ? 2 : 4) <= kGuideL2Keep;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
         ctx.before(hg ? "k_fit_ws_f16" : A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments"
                    : em < 0.0 ? "k_fit_ws_f64acc" : "k_fit_ws");
         const bool acc64 = em < 0.0 && !hg && !A;  // Tikhonov mode (flr_solve.cuh sentinels)
-        if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64);
-        else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64);
-        else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64);
+        if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, ctx.l2_guides);
+        else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, ctx.l2_guides);
+        else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, ctx.l2_guides);
     } else {
         ctx.before("k_moments_small");
         k_moments_small<Q><<<dim3(cdiv(Bx, 128), By, n), 128, 0, s>>>(W, H, Bx, By, D, G, Y, raw);
@@ -291,11 +299,22 @@ void launch_apply(int n, int W, int H, int D, int Bx, int By, const float* model
             const int items = n * a.nseg * a.nband * a.nsub;
             // warp-specialised (one producer warp feeds 7 consumer warps, 2-row stages); faster
             // than per-warp self-feeding rings for one frame and for batches alike
-            using C = ApplyWsCfg<Q>;
-            const int grid = min(num_sms(), cdiv(items, C::NC));
-            ctx.before("k_apply_ws");
-            set_smem(k_apply_ws<Q>, C::SMEM);
-            launch_pdl(k_apply_ws<Q>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+            auto go = [&](auto deep) {
+                constexpr bool DEEP = decltype(deep)::value;
+                using C = ApplyWsCfg<Q, false, false, DEEP>;
+                const int grid = min(num_sms(), cdiv(items, C::NC));
+                ctx.before("k_apply_ws");
+                set_smem(k_apply_ws<Q, false, false, DEEP>, C::SMEM);
+                launch_pdl(k_apply_ws<Q, false, false, DEEP>, dim3(grid), dim3(C::THREADS), C::SMEM, s, a, n);
+            };
+            // (the deep ring only where its stages hold as many rows as the default's: one map)
+            if constexpr (ApplyWsCfg<Q, false, false, true>::RB == ApplyWsCfg<Q>::RB) {
+                if (ctx.l2_guides) {
+                    go(std::true_type{});
+                    return;
+                }
+            }
+            go(std::false_type{});
             return;
         }
         dim3 grid(cdiv(cdiv(W + off, 8), kApplyUnits), cdiv(H + off, kApplyRows), n),

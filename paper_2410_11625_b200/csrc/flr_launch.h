@@ -58,6 +58,8 @@ struct LaunchCtx {
     bool capturing = false;   // stream capture: events become graph event-record nodes
     bool unsupported = false; // set by launchers compiled out of a dev build (FLR_STUB)
     bool early = false;       // FLR_FLAG_INPUTS_READY: the moment grid streams before its grid wait
+    bool keep_guides = false; // the call's apply re-reads the fit's guide planes (denoise, U = 1)
+    bool l2_guides = false;   // ... and the fit left them in L2 (evict_normal): the deep apply ring
     void record()
     {
         if (events && recorded < capacity) {

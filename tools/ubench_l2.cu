@@ -26,6 +26,34 @@ __global__ void __launch_bounds__(1024, 1) k_read(const float4* __restrict__ p, 
     if (acc == 1234.5f) sink[0] = acc;
 }
 
+// The fit's access pattern with plain loads: 8 frames of 11 planar 1920 x 1080 fp32 planes;
+// warp w of the grid takes items (block row by, 128-px segment sg) round robin and reads, for
+// each of the 8 rows and 11 planes, one 512-byte row segment (16 B per lane), SEGW segments
+// wide (SEGW = 1: the kernels' 128-px items; 15: whole 1920-px rows).
+template <int SEGW>
+__global__ void __launch_bounds__(1024, 1) k_items(const float4* __restrict__ p, int nf, float* sink)
+{
+    const int W4 = 1920 / 4, H = 1080, P = 11, nseg = 15 / SEGW;
+    const int per_frame = 135 * nseg, nitems = nf * per_frame;
+    const int lane = threadIdx.x & 31, GW = gridDim.x * (blockDim.x >> 5);
+    float acc = 0.f;
+    for (int it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < nitems; it += GW) {
+        const int f = it / per_frame, rem = it - f * per_frame, by = rem / nseg, sg = rem - by * nseg;
+#pragma unroll 1
+        for (int r = 0; r < 8; ++r) {
+            float4 v[P * SEGW];
+#pragma unroll
+            for (int q = 0; q < P; ++q)
+#pragma unroll
+                for (int u = 0; u < SEGW; ++u)
+                    v[q * SEGW + u] = __ldcs(p + (((size_t)f * P + q) * H + by * 8 + r) * W4 + (sg * SEGW + u) * 32 + lane);
+#pragma unroll
+            for (int q = 0; q < P * SEGW; ++q) acc += v[q].x + v[q].w;
+        }
+    }
+    if (acc == 1234.5f) sink[0] = acc;
+}
+
 int main()
 {
     float* buf;
@@ -51,6 +79,23 @@ int main()
             printf("buffer %5zu MB  threads/SM %4d  %.2f TB/s  (%s)\n", mb, tpb, (double)bytes * passes / (ms * 1e-3) / 1e12,
                    cudaGetErrorString(cudaGetLastError()));
         }
+    }
+    {
+        const int nf = 8;
+        const double bytes = 1920.0 * 1080 * 11 * 4 * nf;
+        auto t = [&](auto kern, const char* name, int tpb) {
+            kern<<<148, tpb>>>(reinterpret_cast<float4*>(buf), nf, sink);
+            cudaEventRecord(e0);
+            kern<<<148, tpb>>>(reinterpret_cast<float4*>(buf), nf, sink);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("fit pattern %-22s threads/SM %4d  %.2f TB/s  (%s)\n", name, tpb, bytes / (ms * 1e-3) / 1e12,
+                   cudaGetErrorString(cudaGetLastError()));
+        };
+        for (int tpb : {256, 512, 1024}) t(k_items<1>, "128-px items", tpb);
+        for (int tpb : {256, 512}) t(k_items<3>, "384-px items", tpb);
     }
     return 0;
 }
