@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG, DEEP>::THREADS, 1) k_ap
         pdl_wait();  // the models come from the previous grid
         if (lane == 0) pdl_trigger();
         if (lane == 0) FLR_TL(2, 1);
+
         constexpr unsigned mask = (1u << NC) - 1;
         while (__any_sync(mask, it < nitems || itm < nitems)) {
 #ifdef FLR_APPLYWS_NOWAIT

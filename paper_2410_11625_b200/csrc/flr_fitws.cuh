@@ -302,8 +302,12 @@ __device__ __forceinline__ void fit_consume_item_rel(const FitArgs& a, int it, i
 #else
         double* out = a.mom + (size_t)f * Dm::KM * cst + (size_t)by * a.Bxp + bx;
 #endif
+        // the moment field is stored (and read by K2) evict_last: the next call rewrites the same
+        // lines, which then stay in L2 instead of being written back under the next fit's
+        // stream (C2 43.05 -> 42.4, 32-frame calls 43.4 -> 42.35 us per frame)
+        const uint64_t mpol = policy_evict_last();
         auto put = [&](int kk, double v) {
-            if (kk % DQ == gi) out[(size_t)kk * cst] = v;
+            if (kk % DQ == gi) st_hint_f64(out + (size_t)kk * cst, v, mpol);
         };
         put(Dm::C_N, nn);
 #pragma unroll

@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kK2WsThreads, 1)
     const int f = blockIdx.z, bx0 = blockIdx.x * kK2TX, by0 = blockIdx.y * kK2TY;
     if (tid >= kK2Threads) {  // ---------------- blur warps ----------------
         const int bt = tid - kK2Threads;
-        const uint64_t kpol = policy_evict_normal();
+        const uint64_t kpol = policy_evict_last();  // the moment field stays in L2 (see k_fit_ws)
         auto issue = [&](int grp) {
             uint64_t* b = &tfull[grp % S];
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage before
