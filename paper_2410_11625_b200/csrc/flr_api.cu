@@ -468,6 +468,7 @@ flr_status flr_denoise_modulated_traced(int32_t n, int32_t Q, int32_t W, int32_t
         const Taps taps = make_taps(sblk, effective_radius(p));
         char* base = (char*)workspace;
         ctx.early = (p->flags & FLR_FLAG_INPUTS_READY) != 0;
+        ctx.keep_guides = true;  // the remodulating apply re-reads these guides (58.5 -> 57.5 us per C2 frame)
         FLR_DISPATCH_Q(Q, (launch_fit<QQ>(n, W, H, D, Bx, By, guides, radiance_mod, (float*)(base + L.raw),
                                           (double*)(base + L.mom), (double*)(base + L.hb), models, ms,
                                           p->eps_add, solver_eps_mul(p), taps, ctx, albedo, albedo_floor)));

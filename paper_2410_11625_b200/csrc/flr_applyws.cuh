@@ -15,6 +15,10 @@
 
 #include "flr_stream.cuh"
 
+#ifndef FLR_OUT_ST
+#define FLR_OUT_ST "st.global.cs.v4.f32"
+#endif
+
 namespace flr {
 
 #ifndef FLR_APPLYWS_NC
@@ -203,7 +207,7 @@ __device__ __forceinline__ void apply_consume_item(const ApplyArgs& a, const App
                 float* Orow = O + (size_t)(ys + r) * a.W + xq;
 #pragma unroll
                 for (int cc = 0; cc < 3; ++cc)
-                    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(Orow + cc * plane),
+                    asm volatile(FLR_OUT_ST " [%0], {%1,%2,%3,%4};" ::"l"(Orow + cc * plane),
                                  "f"(o[r][cc][0]), "f"(o[r][cc][1]), "f"(o[r][cc][2]), "f"(o[r][cc][3])
                                  : "memory");
             }
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(ApplyWsCfg<Q, MOD, HG, DEEP>::THREADS, 1) k_ap
         uint64_t* rempty = rfull + S;
         uint64_t* mfull = rempty + S;
         uint64_t* mempty = mfull + SM;
-        const uint64_t pg = policy_evict_first(), pm = policy_evict_normal();
+                const uint64_t pg = policy_evict_first(), pm = policy_evict_normal();
         // two cursors over the consumer's items: the guide rows (it, y) and the models (itm),
         // which run up to SM items ahead -- a model stage is free as soon as the consumer has
         // its models in registers, so the next item's models are in flight while this one's

@@ -39,10 +39,13 @@ int main(int argc, char** argv)
     cudaStream_t s;
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     const bool noapply = argc > 1 && std::string(argv[argc - 1]) == "noapply";  // fit + K2 only
-    const std::string mode = noapply ? "staged (no apply)" : "staged";
+    const bool early = argc > 1 && std::string(argv[1]) == "early";
+    const std::string mode = std::string(noapply ? "staged (no apply)" : "staged") + (early ? ", inputs ready" : "");
     auto step = [&](int k) {
         LaunchCtx ctx;
         ctx.s = s;
+        ctx.keep_guides = !noapply;  // as flr_denoise: the apply re-reads the fit's guides
+        ctx.early = early;           // FLR_FLAG_INPUTS_READY (argument "early")
         launch_fit<Q>(1, W, H, D, Bx, By, G[k], Y[k], raw, mom, hb, models, Dims<Q>::MSTRIDE, 1e-5, 1e-4, t, ctx);
         if (!noapply) launch_apply<Q>(1, W, H, D, Bx, By, models, Dims<Q>::MSTRIDE, G[k], O[k], ctx);
     };
