@@ -172,17 +172,17 @@ def ncu_traffic(kernel, config):
 
 
 def step_traffic(config, variant, frames):
-    """Whole-step DRAM bytes of one call from the committed ncu app-range capture
+    """Whole-step DRAM bytes per call from the committed ncu app-range capture
     (profiles/r02_step_traffic.json, tools/step_traffic.py), c2 single-frame steps only."""
     p = os.path.join(ROOT, "profiles", "r02_step_traffic.json")
     if config != "c2" or frames != 1 or not os.path.exists(p):
         return None
     try:
-        d = json.load(open(p))["fused" if variant == 2 else "staged"]
+        d = json.load(open(p))["fused" if variant == 2 else "staged_steady"]
         return {"dram_bytes": d["dram_bytes"], "dram_read_bytes": d["dram_read_bytes"],
                 "dram_write_bytes": d["dram_write_bytes"], "bytes_per_output_px": d["dram_bytes_per_output_px"],
-                "source": "profiles/r02_step_traffic.json (ncu app-range replay of one call; write-back of "
-                          "dirty L2 lines after the range is not counted)"}
+                "source": "profiles/r02_step_traffic.json (ncu app-range replay; staged: 8 back-to-back calls "
+                          "without cache flushes, per call, incl. write-backs; fused: one call after a flush)"}
     except Exception:
         return None
 

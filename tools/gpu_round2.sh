@@ -1,9 +1,9 @@
 # round-2 evidence: gpu tests, smoke, bench lines for every config (+ the wave variant and the
-# reference arm), the ncu launch list, one full ncu capture of the dominant kernels, and the
-# whole-step DRAM traffic (ncu app-range replay)
+# reference arm), the ncu launch list, one full ncu capture of the dominant kernels, the
+# whole-step DRAM traffic (ncu app-range replay, steady state over 8 calls), CTA timelines
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.csv 2>&1
-timeout -s KILL 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+timeout -s KILL 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/r02_gpu_tests.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r02_gpu_tests.log
 timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
 timeout -s KILL 900 python bench.py --check > gpurun_out/r02_bench_c2.json 2>gpurun_out/bench_c2.err; echo "bench c2 rc=$?"; tail -c 300 gpurun_out/r02_bench_c2.json
 for X in "--config c1" "--config c3" "--config c4" "--config c5 --steps 20 --warmup 3" "--frames-per-step 8" "--guides f16" "--config c4 --guides f16" "--modulated" "--variant 2"; do
@@ -13,9 +13,6 @@ timeout -s KILL 900 python bench.py --impl reference --steps 20 --warmup 3 > gpu
 CMD="python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 --no-graph"
 timeout -s KILL 300 $CMD > gpurun_out/plain.log 2>&1 && timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"^k_" -s 12 -c 12 --csv --log-file gpurun_out/r02_launches.csv $CMD > gpurun_out/ncu_list.log 2>&1; echo "ncu list rc=$?"
 timeout -s KILL 900 ncu --set full --import-source on --clock-control none -k regex:"k_fit_ws|k_apply_ws|k_blur_solve_tile" -s 6 -c 3 -o gpurun_out/r02_full $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
-for V in staged fused; do
-timeout -s KILL 600 ncu --replay-mode app-range --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum --csv --log-file gpurun_out/r02_step_traffic_$V.csv python tools/step_traffic.py $V > gpurun_out/ncu_step_$V.log 2>&1; echo "ncu step $V rc=$?"
-done
-timeout -s KILL 60 tools/t_timeline > gpurun_out/r02_timeline.txt 2>&1; head -4 gpurun_out/r02_timeline.txt
-# the blur+solve kernel alone (1080p Q=8 R=3 moment field): full capture for shared-memory wavefronts / fp64 pipe
-timeout -s KILL 300 ncu --set full --import-source on --clock-control none -k regex:k_blur_solve_tile -s 5 -c 1 -o gpurun_out/r02_k2 tools/t_k2 1 > gpurun_out/ncu_k2.log 2>&1; echo "ncu k2 rc=$?"
+timeout -s KILL 600 ncu --replay-mode app-range --cache-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum --csv --log-file gpurun_out/r02_step_traffic_staged8.csv python tools/step_traffic.py staged 8 > gpurun_out/ncu_step_staged8.log 2>&1; echo "ncu step staged8 rc=$?"
+timeout -s KILL 600 ncu --replay-mode app-range --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum --csv --log-file gpurun_out/r02_step_traffic_staged.csv python tools/step_traffic.py staged 1 > gpurun_out/ncu_step_staged.log 2>&1; echo "ncu step staged rc=$?"
+(timeout -s KILL 60 tools/t_timeline; timeout -s KILL 60 tools/t_timeline early) > gpurun_out/r02_timeline.txt 2>&1; cat gpurun_out/r02_timeline.txt | grep graph
