@@ -38,8 +38,13 @@ int main(int argc, char** argv)
     for (int i = -3; i <= 3; ++i) t.g[3 + i] = std::exp(-(double)(i * i) / (2.0 * 1.25 * 1.25));
     cudaStream_t s;
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    const bool noapply = argc > 1 && std::string(argv[argc - 1]) == "noapply";  // fit + K2 only
-    const bool early = argc > 1 && std::string(argv[1]) == "early";
+    auto has = [&](const char* a) {
+        for (int i = 1; i < argc; ++i)
+            if (std::string(argv[i]) == a) return true;
+        return false;
+    };
+    const bool noapply = has("noapply");  // fit + K2 only
+    const bool early = has("early");
     const std::string mode = std::string(noapply ? "staged (no apply)" : "staged") + (early ? ", inputs ready" : "");
     auto step = [&](int k) {
         LaunchCtx ctx;
@@ -93,7 +98,7 @@ int main(int argc, char** argv)
         for (int d = 0; d <= 10; ++d) printf(" %.1f", xs[std::min((int)xs.size() - 1, d * (int)xs.size() / 10)]);
         printf("\n");
     }
-    if (argc > 1 && std::string(argv[1]) == "cta") {  // fit: per-CTA exit (relative), SM id, items
+    if (has("cta")) {  // fit: per-CTA exit (relative), SM id, items
         std::vector<std::pair<long long, int>> ex;
         for (int c = 0; c < ncta[0]; ++c) ex.push_back({tl[c * 4 + 2] - t0, c});
         std::sort(ex.begin(), ex.end());
