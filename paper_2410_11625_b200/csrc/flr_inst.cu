@@ -75,8 +75,6 @@ static int num_sms()
 // 8-row bands at D = 8 halve the per-item model copies and producer operations (C2 44.15 vs
 // 44.5 us per frame with 4-row items; the per-SM apply rate 61 vs 51 GB/s at 37 SMs)
 constexpr int kApplySubRows = FLR_APPLY_SUB_ROWS;
-// largest guide volume of one call the fit leaves in L2 (evict_normal) for the apply
-constexpr size_t kGuideL2Keep = (size_t)80 << 20;
 
 // K1: the warp-specialised TMA kernel when the planes allow it, else the tiled kernel
 template <int Q, int D>

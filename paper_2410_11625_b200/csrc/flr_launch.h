@@ -49,6 +49,11 @@ inline int mom_pitch(int Bx) { return (Bx + 1) & ~1; }
 // Per-call launch context: the caller's stream, a launch counter, and an optional
 // caller-owned event trace (events[i] is recorded right before launch i and one
 // more after the last launch; see flr_event_trace in include/flr.h).
+// largest guide volume of one call the fit leaves in L2 (evict_normal) for the apply; batched
+// denoise calls whose frames fit run frame by frame (flr_api.cu)
+constexpr size_t kGuideL2Keep = (size_t)80 << 20;
+constexpr int kMaxLaunchNames = 256;  // launch names kept per call (flr_last_launch_name)
+
 struct LaunchCtx {
     cudaStream_t s = nullptr;
     int launches = 0;
@@ -68,11 +73,11 @@ struct LaunchCtx {
             else cudaEventRecord(e, s);
         }
     }
-    const char* names[16] = {};
+    const char* names[kMaxLaunchNames] = {};
     void before(const char* name)
     {
         record();
-        if (launches < 16) names[launches] = name;
+        if (launches < kMaxLaunchNames) names[launches] = name;
         ++launches;
     }
     void end() { record(); }
