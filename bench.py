@@ -494,8 +494,9 @@ def run_flr(args, cfg, rank, world, local_rank):
         call(i)
     torch.cuda.synchronize()
 
-    # ---- CUDA graphs: a full pool rotation and the remainder (timed), a traced rotation
+    # ---- CUDA graphs: whole pool rotations and the remainder (timed), a traced rotation
     use_graph = not args.no_graph
+    G_STEPS = pool * max(1, -(-32 // pool))  # steps per timed graph
     graphs = {}
     if use_graph:
         side = torch.cuda.Stream(dev)
@@ -514,10 +515,13 @@ def run_flr(args, cfg, rank, world, local_rank):
 
         # the timed graphs carry no events between kernels (an event node would serialise
         # the programmatic-dependent launches); per-kernel durations come from a traced
-        # replay of the same steps right after the timed region
-        reps, rem = divmod(K, pool)
+        # replay of the same steps right after the timed region.  A timed graph holds several
+        # pool rotations (>= 32 steps): the programmatic-dependent chain -- each step's moment
+        # kernel streaming while the previous apply drains -- breaks at every graph launch, as
+        # it would not in a renderer's continuous frame loop
+        reps, rem = divmod(K, G_STEPS)
         if reps:
-            graphs["full"] = capture(pool, False)
+            graphs["full"] = capture(G_STEPS, False)
         if rem:
             graphs["rem"] = capture(rem, False)
         graphs["traced"] = capture(pool, True)
@@ -533,7 +537,7 @@ def run_flr(args, cfg, rank, world, local_rank):
         time.sleep(0.02)
         t_start.record(stream)
         if use_graph:
-            reps, rem = divmod(K, pool)
+            reps, rem = divmod(K, G_STEPS)
             for _ in range(reps):
                 graphs["full"].replay()
             if rem:
@@ -696,7 +700,7 @@ def run_flr(args, cfg, rank, world, local_rank):
         "config": {**ref_config(cfg, R), "frames_per_call": F, "calls_per_step": pool if batch else 1,
                    "global_batch": frames_per_step, "shard": [lo, hi] if batch else None,
                    "pool_frames": pool * F, "l2": f"inputs rotate through {pool * F} distinct resident frames "
-                   f"({pool * F * frame_in_bytes / 1e6:.0f} MB > 126 MB L2)", "graphs": use_graph,
+                   f"({pool * F * frame_in_bytes / 1e6:.0f} MB > 126 MB L2)", "graphs": use_graph, "steps_per_graph": (G_STEPS if use_graph else None),
                    "parallelism": f"frame-sharded dp{world}", "variant": args.variant,
                    "guides": args.guides, "modulated": bool(args.modulated),
                    "flags": "FLR_FLAG_INPUTS_READY" if not args.no_inputs_ready else "0",
