@@ -377,9 +377,9 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
         constexpr int NP = C::NP, LANES = (NC + NP - 1) / NP;
         const int p = warp - NC, c = p + NP * lane;
         if (lane >= LANES || c >= NC) return;
-                // the guides of the bottom 3/4 of the frame (the bottom-up apply reads them first) stay in
-        // L2 when a.gpol asks for it; the top quarter streams (C2 42.35 -> 42.1 us vs all rows)
-        const uint64_t pg = policy_by_code(a.gpol), py = policy_evict_first();
+                // the guide rows from a.keep_y0 down (the bottom-up apply reads them first) stay in L2
+        // (evict_normal); the rows above stream (evict_first) -- see launch_k1
+        const uint64_t pg = policy_evict_normal(), py = policy_evict_first();
         int it = blockIdx.x * NC + c, row = 0, rows = 0, f = 0, by = 0, sg = 0;
         auto decode = [&]() {
             if (it >= nitems) return;
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(FitWsCfg<Q, MOD, HG>::THREADS, 1) k_fit_ws(con
 #endif
                 ws_proxy_fence();
                 fit_issue_row<Q, D, MOD, HG, kFS, C::RB>(a, f, by, sg, row, stages + (size_t)(c * S + slot) * STG,
-                                                         &full[c * S + slot], by * D * 4 >= a.H ? pg : py, py);
+                                                         &full[c * S + slot], by * D >= a.keep_y0 ? pg : py, py);
                 ++k;
                 if ((row += C::RB) >= rows) {
                     row = 0;

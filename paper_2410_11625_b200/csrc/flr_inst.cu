@@ -87,11 +87,13 @@ static void launch_k1(int n, int W, int H, int Bx, int By, const float* G, const
     a.W = W, a.H = H, a.Bx = Bx, a.Bxp = mom_pitch(Bx), a.By = By, a.nseg = cdiv(W, kFS);
     a.afloor = afloor;
     a.early = early;
-    // keep: the apply of this call re-reads these guides.  C2 (66 MB of guides):
-    // evict_normal guides 42.9 vs 43.55 us per frame (the apply's guide re-reads hit L2 more:
-    // -2.8 us; the fit streams next to more dirty lines: +2.2 us); lo-res (C4) and batched
-    // guides stream with evict_first
-    a.gpol = keep ? 1 : 0;
+    // keep: the apply of this call re-reads these guides; the bottom kGuideL2Rows bytes of them
+    // (one frame) stay in L2 for the bottom-up apply.  C2 (66 MB of guides): all rows
+    // evict_normal 42.9 vs 43.55 us per frame (apply -2.8 us; the fit streams next to more
+    // dirty lines: +2.2 us), the bottom 3/4 (= 50 MB) 42.1; lo-res (C4) and batched guides
+    // stream with evict_first
+    const size_t row_bytes = (size_t)Q * W * (hg ? 2 : 4);
+    a.keep_y0 = keep && n == 1 ? H - (int)std::min<size_t>((size_t)H, kGuideL2Rows / row_bytes) : H;
     const int items = n * By * a.nseg;
     if (hg) {  // fp16 guide planes: the warp-specialised kernel with a half-width guide stage
         using C = FitWsCfg<Q, false, true>;
@@ -151,9 +153,10 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
         ctx.before(hg ? "k_fit_ws_f16" : A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments"
                    : em < 0.0 ? "k_fit_ws_f64acc" : "k_fit_ws");
         const bool acc64 = em < 0.0 && !hg && !A;  // Tikhonov mode (flr_solve.cuh sentinels)
-        if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, ctx.l2_guides);
-        else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, ctx.l2_guides);
-        else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, ctx.l2_guides);
+        const bool keep = ctx.keep_guides && !hg;
+        if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, keep);
+        else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, keep);
+        else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, keep);
     } else {
         ctx.before("k_moments_small");
         k_moments_small<Q><<<dim3(cdiv(Bx, 128), By, n), 128, 0, s>>>(W, H, Bx, By, D, G, Y, raw);

@@ -52,6 +52,8 @@ inline int mom_pitch(int Bx) { return (Bx + 1) & ~1; }
 // largest guide volume of one call the fit leaves in L2 (evict_normal) for the apply; batched
 // denoise calls whose frames fit run frame by frame (flr_api.cu)
 constexpr size_t kGuideL2Keep = (size_t)80 << 20;
+// guide bytes of one frame the fit leaves in L2 for the bottom-up apply (its last rows)
+constexpr size_t kGuideL2Rows = (size_t)50 << 20;
 constexpr int kMaxLaunchNames = 256;  // launch names kept per call (flr_last_launch_name)
 
 struct LaunchCtx {

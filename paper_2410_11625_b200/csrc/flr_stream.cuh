@@ -40,9 +40,8 @@ struct FitArgs {
     float afloor;    // albedo floor of the demodulation (modulated fit only)
     int early;       // inputs ready (FLR_FLAG_INPUTS_READY): stream before the grid-dependency
                      // wait, which then only gates this grid's dependents (see k_fit_ws)
-    int gpol;        // L2 policy of the guide reads of the frame's bottom 3/4 (policy_by_code):
-                     // evict_normal when the call's guides fit in L2 next to the moment field, so
-                     // the apply (bottom-up) re-reads many of them from L2; else evict_first
+    int keep_y0;     // guide rows y >= keep_y0 are read evict_normal (the call's bottom-up apply
+                     // re-reads them from L2), the rows above evict_first; H: none
 };
 
 // HG: the guide planes are IEEE binary16 (half the stage bytes of the guides)

@@ -34,7 +34,7 @@ int main()
         FitArgs fa{};
         make_tmap_planes(&fa.tg, G, W, H, nf * Q, kSeg, Q);
         make_tmap_planes(&fa.ty, Y, W, H, nf * 3, kSeg, 3);
-        fa.mom = mom, fa.W = W, fa.H = H, fa.Bx = Bx, fa.Bxp = mom_pitch(Bx), fa.By = By, fa.nseg = W / kSeg;
+        fa.keep_y0 = H, fa.mom = mom, fa.W = W, fa.H = H, fa.Bx = Bx, fa.Bxp = mom_pitch(Bx), fa.By = By, fa.nseg = W / kSeg;
         ApplyArgs aa{};
         make_tmap_planes(&aa.tg, G, W, H, nf * Q, kSeg, Q);
         aa.models = M, aa.out = O, aa.W = W, aa.H = H, aa.D = D, aa.Bx = Bx, aa.By = By;

@@ -107,7 +107,7 @@ int main()
     FitArgs fa{};
     make_tmap_planes(&fa.tg, G, W, H, nf * Q, kFS, Q, FitWsCfg<Q>::RB);
     make_tmap_planes(&fa.ty, Y, W, H, nf * 3, kFS, 3, FitWsCfg<Q>::RB);
-    fa.mom = mom, fa.W = W, fa.H = H, fa.Bx = Bx, fa.Bxp = mom_pitch(Bx), fa.By = By, fa.nseg = W / kFS;
+    fa.keep_y0 = H, fa.mom = mom, fa.W = W, fa.H = H, fa.Bx = Bx, fa.Bxp = mom_pitch(Bx), fa.By = By, fa.nseg = W / kFS;
     ApplyArgs aa{};
     make_tmap_planes(&aa.tg, G, W, H, nf * Q, kSeg, Q, ApplyWsCfg<Q>::RB);
     aa.models = M, aa.out = O, aa.W = W, aa.H = H, aa.D = D, aa.Bx = Bx, aa.By = By;
