@@ -147,13 +147,13 @@ void launch_fit(int n, int W, int H, int D, int Bx, int By, const float* G, cons
                 double em, const Taps& taps, LaunchCtx& ctx, const float* A, float afloor, bool hg)
 {
     const cudaStream_t s = ctx.s;
-    ctx.l2_guides = ctx.keep_guides && (size_t)n * Q * W * H * (hg ? 2 : 4) <= kGuideL2Keep;
+    ctx.l2_guides = ctx.keep_guides && !hg && (size_t)n * Q * W * H * 4 <= kGuideL2Keep;
     // K1: block moments (fp64, un-shifted) -> mom
     if (D >= 4) {
         ctx.before(hg ? "k_fit_ws_f16" : A ? "k_fit_ws_mod" : !vec_ok(G, W) || !vec_ok(Y, W) ? "k_fit_moments"
                    : em < 0.0 ? "k_fit_ws_f64acc" : "k_fit_ws");
         const bool acc64 = em < 0.0 && !hg && !A;  // Tikhonov mode (flr_solve.cuh sentinels)
-        const bool keep = ctx.keep_guides && !hg;
+        const bool keep = ctx.keep_guides;
         if (D == 4) launch_k1<Q, 4>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, keep);
         else if (D == 8) launch_k1<Q, 8>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, keep);
         else launch_k1<Q, 16>(n, W, H, Bx, By, G, Y, mom, s, A, afloor, hg, ctx.early, acc64, keep);

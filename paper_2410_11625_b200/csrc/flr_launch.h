@@ -53,7 +53,10 @@ inline int mom_pitch(int Bx) { return (Bx + 1) & ~1; }
 // denoise calls whose frames fit run frame by frame (flr_api.cu)
 constexpr size_t kGuideL2Keep = (size_t)80 << 20;
 // guide bytes of one frame the fit leaves in L2 for the bottom-up apply (its last rows)
-constexpr size_t kGuideL2Rows = (size_t)50 << 20;
+#ifndef FLR_GUIDE_L2_MB
+#define FLR_GUIDE_L2_MB 50
+#endif
+constexpr size_t kGuideL2Rows = (size_t)FLR_GUIDE_L2_MB << 20;
 constexpr int kMaxLaunchNames = 256;  // launch names kept per call (flr_last_launch_name)
 
 struct LaunchCtx {
