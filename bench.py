@@ -652,11 +652,15 @@ def run_flr(args, cfg, rank, world, local_rank):
     value = px_total / (ms_max * 1e-3) / 1e6
     # dominant kernel (largest share of the step) and its own algorithmic bytes
     known = {n: t for n, t in avg_ms.items() if t}
-    dom = max(known, key=known.get) if known else None
+    # frames one launch of a kernel processes: batched calls whose frames fit in L2 run frame by
+    # frame (one fit / K2 / apply launch per frame), the others one launch per call
+    fpl = {n: F / max(1, kernel_names.count(n)) for n in known}
+    # dominant kernel: the largest share of the step (launch time x launches per call)
+    dom = max(known, key=lambda n: known[n] * kernel_names.count(n)) if known else None
     roof = None
     if dom:
         bytes_fn = KERNEL_BYTES.get(dom)
-        alg = bytes_fn(cfg) * F if bytes_fn else None
+        alg = bytes_fn(cfg) * fpl[dom] if bytes_fn else None
         if alg is not None:
             ach = alg / (known[dom] * 1e-3) / 1e9
             roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
@@ -664,7 +668,7 @@ def run_flr(args, cfg, rank, world, local_rank):
                     "algorithmic_bytes_per_launch": alg, "avg_launch_us": known[dom] * 1e3,
                     "peak_source": peak_src}
         elif dom in KERNEL_FLOPS:
-            ach = KERNEL_FLOPS[dom](cfg) * F / (known[dom] * 1e-3) / 1e12
+            ach = KERNEL_FLOPS[dom](cfg) * fpl[dom] / (known[dom] * 1e-3) / 1e12
             roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": FP64_PEAK_TFLOPS,
                     "unit": "TFLOP/s (fp64)", "frac": ach / FP64_PEAK_TFLOPS, "traffic": ncu_traffic(dom, args.config),
                     "avg_launch_us": known[dom] * 1e3, "peak_source": "derived: 148 SM x 64 DFMA/clk x 1.965 GHz"}
@@ -675,11 +679,11 @@ def run_flr(args, cfg, rank, world, local_rank):
     kroof = {}
     for n, t in known.items():
         if n in KERNEL_BYTES:
-            a_ = KERNEL_BYTES[n](cfg) * F / (t * 1e-3) / 1e9
+            a_ = KERNEL_BYTES[n](cfg) * fpl[n] / (t * 1e-3) / 1e9
             kroof[n] = {"bound": "hbm", "achieved": a_, "peak": peak, "unit": "GB/s", "frac": a_ / peak,
                         "avg_launch_us": t * 1e3}
         elif n in KERNEL_FLOPS:
-            a_ = KERNEL_FLOPS[n](cfg) * F / (t * 1e-3) / 1e12
+            a_ = KERNEL_FLOPS[n](cfg) * fpl[n] / (t * 1e-3) / 1e12
             kroof[n] = {"bound": "alu", "achieved": a_, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s (fp64)",
                         "frac": a_ / FP64_PEAK_TFLOPS, "avg_launch_us": t * 1e3}
     step_ms = ms_max / args.steps  # c5: one pass over the rank's shard of the batch

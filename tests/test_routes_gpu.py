@@ -60,3 +60,29 @@ def test_fit_packed_models(oracle_mod, Q):
     got = oracle_mod.apply(m.cpu().numpy(), G.numpy(), 8)
     ref = oracle_mod.denoise(G.numpy(), Y.numpy(), D=8, sigma=10.0, R=3)
     assert_parity(got, ref, f"flr_fit Q={Q} through the oracle apply")
+
+
+@pytest.mark.parametrize("W,H,n", [(640, 360, 5), (1032, 264, 3)])
+def test_batched_denoise_runs_frame_by_frame(oracle_mod, W, H, n):
+    """A batched denoise whose frames fit in L2 runs fit -> K2 -> apply per frame (flr_api.cu,
+    DESIGN section 7): 3 launches per frame, each frame bitwise equal to a single-frame call
+    (same kernels, same arithmetic), and the oracle bar on first, middle and last frames."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2410_11625_b200 as flr
+    from paper_2410_11625_b200 import synth
+
+    G, Y = synth.batch(n, W, H, Q=8, seed0=7300 + W)
+    g, y = G.cuda(), Y.cuda()
+    out = flr.denoise(g, y)
+    torch.cuda.synchronize()
+    names = flr.last_launch_names()
+    assert names == ["k_fit_ws", "k_blur_solve_tile", "k_apply_ws"] * n, names
+    for f in range(n):
+        single = flr.denoise(g[f:f + 1].contiguous(), y[f:f + 1].contiguous())
+        torch.cuda.synchronize()
+        assert torch.equal(out[f:f + 1], single), f"frame {f} differs from its single-frame call"
+    R = flr.effective_radius(block=8, sigma=10.0)
+    for f in (0, n // 2, n - 1):
+        ref = oracle_mod.denoise(G[f:f + 1].numpy(), Y[f:f + 1].numpy(), D=8, sigma=10.0, R=R)
+        assert_parity(out[f:f + 1].cpu().numpy(), ref, f"batched frame {f}")
